@@ -1,0 +1,39 @@
+"""Oracle prefix forward: y = f_s o ... o f_1 (x), each image independently.
+
+TEST INFRASTRUCTURE ONLY (see oracle/ops.py header).
+
+This is the storage-side hot path's definition: the server "executes the feature
+extraction part up to the split index" and "sends back the outputs of the split
+index layer", using "custom DNN models that run the forward pass
+between arbitrary start and end layers".  Split index s = number of
+leading layers run on storage, 1-based, inclusive (reading R1/A1).  The output is
+the layer-s tensor for the whole batch, NCHW (or [b, F] inside a classifier) --
+reading R11/A18.  Accumulation is float64.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import archs
+
+
+def prefix_forward(arch: str, params, images: np.ndarray, split_idx: int) -> np.ndarray:
+    mods = archs.layers(arch)
+    if not 1 <= split_idx <= len(mods):
+        raise ValueError(f"split_idx {split_idx} not in [1, {len(mods)}]")
+    x = np.asarray(images, dtype=np.float64)
+    for m in mods[:split_idx]:
+        x = m.fwd(x, params)
+    return x
+
+
+def prefix_forward_all(arch: str, params, images: np.ndarray, upto: int | None = None):
+    """Outputs of every layer 1..upto (one pass; used by the profiling-run pin)."""
+    mods = archs.layers(arch)
+    upto = len(mods) if upto is None else upto
+    x = np.asarray(images, dtype=np.float64)
+    outs = []
+    for m in mods[:upto]:
+        x = m.fwd(x, params)
+        outs.append(x)
+    return outs
