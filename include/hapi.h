@@ -1,0 +1,195 @@
+/*
+ * hapi.h -- C ABI of the B200-native storage-side prefix forward of HAPI
+ * (Guirguis et al., "Accelerating Transfer Learning with Near-Data Computation on
+ * Cloud Object Stores", arXiv 2210.08650).  PAPER.md below = /root/reference/PAPER.md.
+ *
+ * The hot path: the storage side "reads the object that holds the training data and
+ * the specified DNN ... and then executes the feature extraction part up to the split
+ * index" and "sends back the outputs of the split index layer" (section 4.1,
+ * PAPER.md:732-734), running "custom DNN models that run the forward pass between
+ * arbitrary start and end layers".  The planner calls follow the
+ * paper's statement of the problem: per-layer output sizes and the memory profile
+ * (section 4.3), the split index (Alg. 1) and the
+ * storage-side (COS) batch size under a GPU-memory budget (Eq. 4).
+ *
+ * Conventions (all calls):
+ *   - Plain C types; pointers are host pointers unless documented as device.
+ *   - Return HAPI_OK (0) or a positive hapi_status; hapi_last_error() returns a
+ *     thread-local message for the last failure on the calling thread.
+ *   - Layer indices s are 1-based and inclusive: s = number of leading layers run on
+ *     storage (L_COS, Appendix C; reading R1).  Array slot
+ *     [s-1] describes layer s.
+ *   - Layers are the canonical torchvision module lists of DESIGN.md reading R2
+ *     (AlexNet 21, ResNet18 14, ResNet50 22, VGG11 29, DenseNet121 22).
+ */
+#ifndef HAPI_H_
+#define HAPI_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HAPI_API __attribute__((visibility("default")))
+#else
+#define HAPI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HAPI_OK = 0,
+  HAPI_ERR_INVALID_ARGUMENT = 1, /* batch 0, split/freeze out of range, link 0, b_min > b_max,
+                                    capacity < L, u64 overflow, null pointer */
+  HAPI_ERR_INVALID_MODEL = 2,    /* unknown arch, params count/shape mismatch, image size too small */
+  HAPI_ERR_INFEASIBLE = 3,       /* the HBM budget cannot hold b_min images (Eq. 4 has no solution;
+                                    the single-request analog of "removes one request ... and
+                                    retries") */
+  HAPI_ERR_OUT_OF_MEMORY = 4,    /* device allocation failed */
+  HAPI_ERR_CUDA = 5,             /* a CUDA runtime/driver call failed (incl. earlier async faults) */
+  HAPI_ERR_UNSUPPORTED = 6       /* valid request this build does not implement */
+} hapi_status;
+
+typedef enum { HAPI_ALEXNET = 0, HAPI_RESNET18 = 1, HAPI_RESNET50 = 2, HAPI_VGG11 = 3,
+               HAPI_DENSENET121 = 4 } hapi_arch;
+
+/* Activation dtype of the prefix.  F32: fp32 activations, fp32 SIMT math (the paper's
+ * precision, reading R7).  BF16: bf16 activations, fp32 accumulation on tcgen05 tensor
+ * cores.  Images are always fp32 NCHW. */
+typedef enum { HAPI_F32 = 0, HAPI_BF16 = 1 } hapi_dtype;
+
+/* ------------------------------------------------------------------ planner (host) */
+
+/* Number of canonical layers L of `arch`, or -HAPI_ERR_INVALID_MODEL. Pure. */
+HAPI_API int32_t hapi_num_layers(hapi_arch arch);
+
+/* Table 2 freeze index of `arch`, or -HAPI_ERR_INVALID_MODEL. Pure. */
+HAPI_API int32_t hapi_freeze_index(hapi_arch arch);
+
+/* Per-layer facts for s = 1..L (slot s-1); Alg. 1 profile_model
+ * computed analytically (shapes are static, so no profiling run is needed):
+ *   input_bytes  l0 = 3*in_h*in_w*4   (the fp32 input sample, Alg. 1 line 9; reading A3)
+ *   out_bytes    l_s = numel(output of layer s) * sizeof(act)
+ *   peak_bytes   P(s) = max_{1<=i<=s} (l_{i-1} + l_i)   ("maximum input plus output size
+ *                across all layers", section 4.3)
+ *   weight_bytes W(s) = sum_{i<=s} weight elems*sizeof(act) + (bias + BN gamma,beta elems)*4
+ * Any output pointer may be NULL.  capacity = length of the caller's arrays (>= L).
+ * Pure, re-entrant, no device work.  Errors: INVALID_MODEL (arch, or an empty layer
+ * output at this image size), INVALID_ARGUMENT (capacity < L, overflow). */
+HAPI_API hapi_status hapi_layer_sizes(hapi_arch arch, uint32_t in_h, uint32_t in_w, hapi_dtype act,
+                             uint64_t *input_bytes, uint64_t *out_bytes, uint64_t *peak_bytes,
+                             uint64_t *weight_bytes, uint32_t capacity);
+
+typedef struct {
+  hapi_arch arch;
+  uint32_t in_h, in_w;        /* image size (224 x 224 for ImageNet, reading R6) */
+  hapi_dtype act;             /* sizes are counted in this dtype */
+  uint32_t freeze_idx;        /* 1..L; Table 2 defaults 17, 11, 21, 25, 20 */
+  uint64_t training_batch;    /* >= 1 */
+  uint64_t link_bytes_per_s;  /* > 0; 1 Gbps = 125,000,000 B/s (reading A4) */
+  uint32_t threshold_ms;      /* >= 1; 1000 = "network bandwidth times 1s" */
+  uint64_t hbm_budget_bytes;  /* memory the storage side may use on this GPU
+                                 (M_total - M_occupied of Eq. 4) */
+  uint32_t b_min, b_max;      /* COS batch bounds: b_min = 25; b_max <= training
+                                 batch. 1 <= b_min <= b_max */
+} hapi_split_query;
+
+typedef struct {
+  uint32_t split_idx;           /* Alg. 1 winner in 1..freeze_idx */
+  uint32_t cos_batch;           /* min(b_max, floor((budget - W(s)) / P(s))); 0 if infeasible */
+  uint64_t bytes_per_iteration; /* l_split * training_batch */
+  uint64_t est_bytes;           /* W(s) + cos_batch * P(s) */
+  uint32_t n_candidates;        /* |{l <= freeze : l_l < l0}| */
+} hapi_split_result;
+
+/* Alg. 1 choose_split_idx + Eq. 4 for one request:
+ *   candidates = {l <= freeze : l_l < l0} ascending; C = link_bytes_per_s*threshold_ms/1000;
+ *   split = first candidate with l_l * training_batch < C, else freeze_idx (both
+ *   comparisons strict, reading A5; line 16 read as `winner = l`, reading A6);
+ *   cos_batch = largest b in [b_min, b_max] with W(s) + b*P(s) <= budget.
+ * `candidates` (optional, may be NULL) receives n_candidates indices; it must hold L.
+ * Returns HAPI_ERR_INFEASIBLE with r fully filled (cos_batch = 0, est = W(s)) when b_min
+ * does not fit.  All arithmetic u64 with overflow -> INVALID_ARGUMENT.  Pure. */
+HAPI_API hapi_status hapi_choose_split(const hapi_split_query *q, hapi_split_result *r, uint32_t *candidates);
+
+/* Parameters expected by hapi_model_create, in torchvision state_dict order
+ * (num_batches_tracked buffers excluded): count, and per index the name (copied into
+ * name_buf, NUL-terminated, truncated to name_cap) and shape (dims[4], *ndim). */
+HAPI_API int32_t hapi_num_params(hapi_arch arch);
+HAPI_API hapi_status hapi_param_info(hapi_arch arch, uint32_t idx, char *name_buf, uint32_t name_cap,
+                            int64_t dims[4], uint32_t *ndim);
+
+/* ------------------------------------------------------------------ executor (device) */
+
+typedef struct hapi_model hapi_model;
+
+typedef struct {
+  hapi_arch arch;
+  hapi_dtype act;
+  uint32_t in_h, in_w;       /* image size; 224 x 224 for every config (reading R6) */
+  uint32_t min_split, max_split; /* plans are prepared for split_idx in [min_split, max_split],
+                                    1 <= min <= max <= L; weights of layers 1..max_split are
+                                    kept on the device */
+  uint32_t max_batch;        /* arena sized for this many images per launch (normally the
+                                 cos_batch of hapi_choose_split); larger calls are chunked */
+  int device;                /* CUDA ordinal */
+} hapi_model_desc;
+
+/* Builds a model: reads the fp32 host params (read during the call only; caller keeps
+ * ownership), folds eval-mode BatchNorm into the preceding conv in fp64 where the plan
+ * allows it, converts/packs weights for the kernels, uploads them, allocates the arena
+ * and builds one launch plan per split.  Errors: INVALID_ARGUMENT (desc), INVALID_MODEL
+ * (n_params != hapi_num_params, unsupported image size), OUT_OF_MEMORY, CUDA. */
+HAPI_API hapi_status hapi_model_create(const hapi_model_desc *desc, const float *const *params,
+                              uint32_t n_params, hapi_model **m);
+
+/* Stream for subsequent launches (a cudaStream_t; NULL = legacy default stream). */
+HAPI_API hapi_status hapi_model_set_stream(hapi_model *m, void *cuda_stream);
+
+/* The hot path.  images: DEVICE pointer, [batch,3,in_h,in_w] fp32 NCHW contiguous.
+ * out: DEVICE pointer with room for batch * out_bytes[split_idx-1] bytes; receives the
+ * layer-split_idx activations as contiguous NCHW [batch,C,H,W] (or [batch,F] inside a
+ * classifier) in the model's act dtype (reading R11).  Images are processed in chunks
+ * of max_batch in order; results do not depend on chunking (a8).  Asynchronous on the
+ * model's stream; never allocates.  images/out must not alias each other or the model.
+ * Errors: INVALID_ARGUMENT (batch 0, split outside [min_split,max_split], null),
+ * CUDA (launch failure or an earlier asynchronous fault). */
+HAPI_API hapi_status hapi_prefix_forward(hapi_model *m, uint32_t split_idx, const float *images,
+                                uint64_t batch, void *out);
+
+/* End-to-end variant with HOST buffers (pinned or pageable): images [batch,3,H,W] fp32
+ * host -> device copies, prefix forward, device -> host copy of the split output into
+ * host `out`, pipelined in max_batch chunks over two streams (H2D of chunk i+1 overlaps
+ * compute of chunk i).  Synchronous: returns when `out` is filled. */
+HAPI_API hapi_status hapi_prefix_forward_host(hapi_model *m, uint32_t split_idx, const float *images,
+                                     uint64_t batch, void *out);
+
+/* Device bytes owned by the model: packed weights (+bias/BN vectors) and the arena. */
+HAPI_API hapi_status hapi_model_device_bytes(const hapi_model *m, uint64_t *weight_bytes, uint64_t *arena_bytes);
+
+/* Per-launch profile of split_idx's plan (for bench.py's roofline): number of kernel
+ * launches per chunk, and for launch i (< cap): a kernel-class id (0 conv_tc, 1 conv_simt,
+ * 2 pool, 3 pack, 4 eltwise), algorithmic FLOPs and algorithmic bytes per image. */
+HAPI_API hapi_status hapi_plan_info(const hapi_model *m, uint32_t split_idx, uint32_t *n_launches,
+                           uint32_t *kind, double *flops_per_img, double *bytes_per_img,
+                           uint32_t cap);
+
+/* Same as hapi_prefix_forward on one chunk (batch <= max_batch), recording a CUDA event
+ * before and after every launch; per-launch milliseconds are written to ms[i] (< cap)
+ * after an internal stream synchronize.  Instrumentation for measurement only. */
+HAPI_API hapi_status hapi_prefix_forward_timed(hapi_model *m, uint32_t split_idx, const float *images,
+                                      uint64_t batch, void *out, float *ms, uint32_t cap);
+
+HAPI_API void hapi_model_destroy(hapi_model *m);
+
+/* Thread-local message describing the last error on this thread ("" if none). */
+HAPI_API const char *hapi_last_error(void);
+
+/* Build identification string (compile target, version). */
+HAPI_API const char *hapi_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HAPI_H_ */

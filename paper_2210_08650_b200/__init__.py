@@ -1,0 +1,163 @@
+"""HAPI (arXiv 2210.08650) storage-side prefix forward, B200-native.
+
+Python face of the C ABI in include/hapi.h (same names, argument marshalling only).
+PyTorch is used for device memory and streams; all compute runs in libhapi.so
+(tcgen05/TMEM/TMA implicit-GEMM convolutions for bf16, SIMT FFMA for fp32).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+from . import _lib
+from ._lib import SplitQuery, lib  # noqa: F401
+
+ARCHS = {"alexnet": 0, "resnet18": 1, "resnet50": 2, "vgg11": 3, "densenet121": 4}
+DTYPES = {"f32": 0, "bf16": 1}
+STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "INVALID_MODEL", 3: "INFEASIBLE", 4: "OUT_OF_MEMORY", 5: "CUDA",
+          6: "UNSUPPORTED"}
+
+
+class HapiError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"HAPI_ERR_{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st: int):
+    if st != 0:
+        raise HapiError(st, _lib.hapi_last_error().decode())
+
+
+def _arch(a) -> int:
+    return ARCHS[a] if isinstance(a, str) else int(a)
+
+
+def _dt(d) -> int:
+    return DTYPES[d] if isinstance(d, str) else int(d)
+
+
+def build_info() -> str:
+    return _lib.hapi_build_info().decode()
+
+
+def hapi_num_layers(arch) -> int:
+    n = _lib.hapi_num_layers(_arch(arch))
+    if n < 0:
+        raise HapiError(-n, "unknown arch")
+    return n
+
+
+def hapi_freeze_index(arch) -> int:
+    return _lib.hapi_freeze_index(_arch(arch))
+
+
+def hapi_layer_sizes(arch, in_h: int = 224, in_w: int = 224, act="f32"):
+    """-> (l0, out_bytes[L], peak_bytes[L], weight_bytes[L])"""
+    L = hapi_num_layers(arch)
+    o, p, w, l0 = (_lib.u64 * L)(), (_lib.u64 * L)(), (_lib.u64 * L)(), _lib.u64()
+    _check(_lib.hapi_layer_sizes(_arch(arch), in_h, in_w, _dt(act), C.byref(l0), o, p, w, L))
+    return l0.value, list(o), list(p), list(w)
+
+
+def hapi_choose_split(arch, freeze_idx: int, training_batch: int, link_bytes_per_s: int, hbm_budget_bytes: int,
+                      b_min: int = 25, b_max: int = 2000, threshold_ms: int = 1000, act="f32", in_h: int = 224,
+                      in_w: int = 224, raise_infeasible: bool = False):
+    """Alg. 1 + Eq. 4.  Returns (status, SplitResult-as-dict, candidates)."""
+    L = hapi_num_layers(arch)
+    q = SplitQuery(_arch(arch), in_h, in_w, _dt(act), freeze_idx, training_batch, link_bytes_per_s, threshold_ms,
+                   hbm_budget_bytes, b_min, b_max)
+    r = _lib.SplitResult()
+    cands = (_lib.u32 * L)()
+    st = _lib.hapi_choose_split(C.byref(q), C.byref(r), cands)
+    if st not in (0, 3) or (st == 3 and raise_infeasible):
+        _check(st)
+    res = dict(split_idx=r.split_idx, cos_batch=r.cos_batch, bytes_per_iteration=r.bytes_per_iteration,
+               est_bytes=r.est_bytes, n_candidates=r.n_candidates)
+    return ("ok" if st == 0 else "infeasible"), res, list(cands)[: r.n_candidates]
+
+
+def hapi_param_table(arch):
+    """[(name, shape)] the library expects, in torchvision state_dict order."""
+    n = _lib.hapi_num_params(_arch(arch))
+    out = []
+    buf = C.create_string_buffer(256)
+    dims = (_lib.i64 * 4)()
+    nd = _lib.u32()
+    for i in range(n):
+        _check(_lib.hapi_param_info(_arch(arch), i, buf, 256, dims, C.byref(nd)))
+        out.append((buf.value.decode(), tuple(dims[: nd.value])))
+    return out
+
+
+class Model:
+    """hapi_model handle.  `params`: sequence of fp32 C-contiguous arrays (numpy or CPU
+    torch tensors) in hapi_param_table order."""
+
+    def __init__(self, arch, act, params: Sequence, max_batch: int, min_split: int, max_split: Optional[int] = None,
+                 in_h: int = 224, in_w: int = 224, device: int = 0):
+        import numpy as np
+        max_split = min_split if max_split is None else max_split
+        self.arch, self.act = arch, act
+        self.in_h, self.in_w, self.max_batch = in_h, in_w, max_batch
+        self.min_split, self.max_split = min_split, max_split
+        keep = [np.ascontiguousarray(np.asarray(p, dtype=np.float32)) for p in params]
+        ptrs = (C.c_void_p * len(keep))(*[p.ctypes.data for p in keep])
+        d = _lib.ModelDesc(_arch(arch), _dt(act), in_h, in_w, min_split, max_split, max_batch, device)
+        h = C.c_void_p()
+        _check(_lib.hapi_model_create(C.byref(d), ptrs, len(keep), C.byref(h)))
+        self._h = h
+        self.device = device
+        self.out_bytes = hapi_layer_sizes(arch, in_h, in_w, act)[1]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.hapi_model_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_stream(self, stream_ptr: int):
+        _check(_lib.hapi_model_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def out_shape(self, split_idx: int, batch: int):
+        return batch, self.out_bytes[split_idx - 1] // (4 if self.act == "f32" else 2)
+
+    def forward(self, split_idx: int, images, out):
+        """images: CUDA fp32 [batch,3,H,W] contiguous tensor; out: CUDA tensor with room
+        for the split output (act dtype).  Launches on the model's stream."""
+        assert images.is_cuda and images.is_contiguous() and out.is_cuda and out.is_contiguous()
+        _check(_lib.hapi_prefix_forward(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
+                                        C.c_void_p(out.data_ptr())))
+        return out
+
+    def forward_host(self, split_idx: int, images, out):
+        """HOST buffers (numpy or CPU tensors); synchronous end-to-end call."""
+        ip = images.ctypes.data if hasattr(images, "ctypes") else images.data_ptr()
+        op = out.ctypes.data if hasattr(out, "ctypes") else out.data_ptr()
+        _check(_lib.hapi_prefix_forward_host(self._h, split_idx, C.c_void_p(ip), images.shape[0], C.c_void_p(op)))
+        return out
+
+    def forward_timed(self, split_idx: int, images, out) -> List[float]:
+        n = self.plan_info(split_idx)["n"]
+        ms = (C.c_float * n)()
+        _check(_lib.hapi_prefix_forward_timed(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
+                                              C.c_void_p(out.data_ptr()), ms, n))
+        return list(ms)
+
+    def device_bytes(self):
+        w, a = _lib.u64(), _lib.u64()
+        _check(_lib.hapi_model_device_bytes(self._h, C.byref(w), C.byref(a)))
+        return w.value, a.value
+
+    def plan_info(self, split_idx: int):
+        n = _lib.u32()
+        _check(_lib.hapi_plan_info(self._h, split_idx, C.byref(n), None, None, None, 0))
+        k = (_lib.u32 * n.value)()
+        fl = (C.c_double * n.value)()
+        by = (C.c_double * n.value)()
+        _check(_lib.hapi_plan_info(self._h, split_idx, C.byref(n), k, fl, by, n.value))
+        return dict(n=n.value, kind=list(k), flops=list(fl), bytes=list(by))
+
+
+KERNEL_CLASSES = {0: "conv_tc", 1: "conv_simt", 2: "pool", 3: "pack", 4: "eltwise"}

@@ -1,0 +1,66 @@
+"""Thin ctypes binding of include/hapi.h.  Argument marshalling only: every step of
+the hot path runs inside libhapi.so.  There is no CPU fallback -- if the library is
+missing this module raises at import time."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libhapi.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2210_08650_b200.build` "
+                      "(there is no CPU fallback for the HAPI prefix forward)")
+lib = C.CDLL(LIB_PATH)
+
+u32, u64, i32, i64 = C.c_uint32, C.c_uint64, C.c_int32, C.c_int64
+P_u64, P_u32, P_dbl, P_f32 = C.POINTER(u64), C.POINTER(u32), C.POINTER(C.c_double), C.POINTER(C.c_float)
+
+
+class SplitQuery(C.Structure):
+    _fields_ = [("arch", C.c_int), ("in_h", u32), ("in_w", u32), ("act", C.c_int), ("freeze_idx", u32),
+                ("training_batch", u64), ("link_bytes_per_s", u64), ("threshold_ms", u32),
+                ("hbm_budget_bytes", u64), ("b_min", u32), ("b_max", u32)]
+
+
+class SplitResult(C.Structure):
+    _fields_ = [("split_idx", u32), ("cos_batch", u32), ("bytes_per_iteration", u64), ("est_bytes", u64),
+                ("n_candidates", u32)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("arch", C.c_int), ("act", C.c_int), ("in_h", u32), ("in_w", u32), ("min_split", u32),
+                ("max_split", u32), ("max_batch", u32), ("device", C.c_int)]
+
+
+def _sig(name, res, *args):
+    f = getattr(lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+hapi_num_layers = _sig("hapi_num_layers", i32, C.c_int)
+hapi_freeze_index = _sig("hapi_freeze_index", i32, C.c_int)
+hapi_layer_sizes = _sig("hapi_layer_sizes", C.c_int, C.c_int, u32, u32, C.c_int, P_u64, P_u64, P_u64, P_u64, u32)
+hapi_choose_split = _sig("hapi_choose_split", C.c_int, C.POINTER(SplitQuery), C.POINTER(SplitResult), P_u32)
+hapi_num_params = _sig("hapi_num_params", i32, C.c_int)
+hapi_param_info = _sig("hapi_param_info", C.c_int, C.c_int, u32, C.c_char_p, u32, C.POINTER(i64), P_u32)
+hapi_model_create = _sig("hapi_model_create", C.c_int, C.POINTER(ModelDesc), C.POINTER(C.c_void_p), u32,
+                         C.POINTER(C.c_void_p))
+hapi_model_set_stream = _sig("hapi_model_set_stream", C.c_int, C.c_void_p, C.c_void_p)
+hapi_prefix_forward = _sig("hapi_prefix_forward", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
+hapi_prefix_forward_host = _sig("hapi_prefix_forward_host", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
+hapi_model_device_bytes = _sig("hapi_model_device_bytes", C.c_int, C.c_void_p, P_u64, P_u64)
+hapi_plan_info = _sig("hapi_plan_info", C.c_int, C.c_void_p, u32, P_u32, P_u32, P_dbl, P_dbl, u32)
+hapi_prefix_forward_timed = _sig("hapi_prefix_forward_timed", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p,
+                                 P_f32, u32)
+hapi_model_destroy = _sig("hapi_model_destroy", None, C.c_void_p)
+hapi_last_error = _sig("hapi_last_error", C.c_char_p)
+hapi_build_info = _sig("hapi_build_info", C.c_char_p)
+
+EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_choose_split", "hapi_num_params",
+            "hapi_param_info", "hapi_model_create", "hapi_model_set_stream", "hapi_prefix_forward",
+            "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_prefix_forward_timed",
+            "hapi_model_destroy", "hapi_last_error", "hapi_build_info"]

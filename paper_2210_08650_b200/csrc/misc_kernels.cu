@@ -1,0 +1,270 @@
+// Memory-bound kernels of the hot path:
+//   pack_input   a1: caller NCHW fp32 images -> NHWC activations (bf16 padded to C=4)
+//   pool         a4: max 3x3/s2 (-inf padding), max 2x2/s2, avg 2x2/s2 (DenseNet transitions)
+//   adaptive     a4: adaptive / global average pool (ResNet avgpool, DenseNet classifier)
+//   bn_act       a5: unfused eval BN (+ReLU) at split points inside a DenseNet transition,
+//                    norm5, and strided channel copies into a DenseNet block buffer
+//   pack_output  a7: NHWC activation -> the contiguous NCHW send buffer
+// All are coalesced along channels with 16-byte vector accesses where alignment allows.
+#include <cuda_bf16.h>
+
+#include "kernels.h"
+
+namespace hapi {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float to_f(T v);
+template <>
+__device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// V consecutive elements of T (16 bytes when V*sizeof(T) == 16).
+template <typename T, int V>
+struct Vec {
+  T v[V];
+};
+template <typename T, int V>
+__device__ __forceinline__ void load_vec(const T* p, float (&f)[V]) {
+  if constexpr (V * sizeof(T) == 16) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const Vec<T, V> t = *reinterpret_cast<const Vec<T, V>*>(&u);
+#pragma unroll
+    for (int i = 0; i < V; ++i) f[i] = to_f<T>(t.v[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) f[i] = to_f<T>(p[i]);
+  }
+}
+template <typename T, int V>
+__device__ __forceinline__ void store_vec(T* p, const float (&f)[V]) {
+  if constexpr (V * sizeof(T) == 16) {
+    Vec<T, V> t;
+#pragma unroll
+    for (int i = 0; i < V; ++i) t.v[i] = from_f<T>(f[i]);
+    *reinterpret_cast<uint4*>(p) = *reinterpret_cast<const uint4*>(&t);
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; ++i) p[i] = from_f<T>(f[i]);
+  }
+}
+
+// ---------------------------------------------------------------- pack_input
+__global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int HW, int is_bf16) {
+  const long long total = (long long)N * HW;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long n = i / HW;
+    const long long p = i - n * HW;
+    const float* src = img + n * 3 * HW + p;
+    const float r = __ldg(src), g = __ldg(src + HW), b = __ldg(src + 2 * HW);
+    if (is_bf16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(r, g);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(b, 0.f);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&lo);
+      o.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(y)[i] = o;
+    } else {
+      float* yo = static_cast<float*>(y) + i * 3;
+      yo[0] = r; yo[1] = g; yo[2] = b;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- pooling
+template <typename T, int V>
+__global__ void pool_kernel(const PoolArgs a) {
+  const int cg = a.C / V;
+  const long long total = (long long)a.N * a.OH * a.OW * cg;
+  const T* x = static_cast<const T*>(a.x);
+  T* y = static_cast<T*>(a.y);
+  const float inv = 1.f / (float)(a.k * a.k);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % cg) * V;
+    const long long pix = i / cg;
+    const int ow = (int)(pix % a.OW);
+    const int oh = (int)((pix / a.OW) % a.OH);
+    const long long n = pix / ((long long)a.OW * a.OH);
+    float acc[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[j] = a.mode == 0 ? -INFINITY : 0.f;
+    for (int r = 0; r < a.k; ++r) {
+      const int ih = oh * a.stride - a.pad + r;
+      if ((unsigned)ih >= (unsigned)a.H) continue;
+      for (int s = 0; s < a.k; ++s) {
+        const int iw = ow * a.stride - a.pad + s;
+        if ((unsigned)iw >= (unsigned)a.W) continue;
+        float f[V];
+        load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] = a.mode == 0 ? fmaxf(acc[j], f[j]) : acc[j] + f[j];
+      }
+    }
+    if (a.mode == 1) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc[j] *= inv;
+    }
+    store_vec<T, V>(y + pix * a.y_ld + c, acc);
+  }
+}
+
+template <typename T, int V>
+__global__ void adaptive_kernel(const AdaptiveArgs a) {
+  const int cg = a.C / V;
+  const long long total = (long long)a.N * a.OH * a.OW * cg;
+  const T* x = static_cast<const T*>(a.x);
+  T* y = static_cast<T*>(a.y);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % cg) * V;
+    const long long pix = i / cg;
+    const int ow = (int)(pix % a.OW);
+    const int oh = (int)((pix / a.OW) % a.OH);
+    const long long n = pix / ((long long)a.OW * a.OH);
+    // PyTorch bins: [floor(i*H/o), ceil((i+1)*H/o))
+    const int h0 = (oh * a.H) / a.OH, h1 = ((oh + 1) * a.H + a.OH - 1) / a.OH;
+    const int w0 = (ow * a.W) / a.OW, w1 = ((ow + 1) * a.W + a.OW - 1) / a.OW;
+    float acc[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[j] = 0.f;
+    for (int ih = h0; ih < h1; ++ih)
+      for (int iw = w0; iw < w1; ++iw) {
+        float f[V];
+        load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f);
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[j] += a.relu_in ? fmaxf(f[j], 0.f) : f[j];
+      }
+    const float inv = 1.f / (float)((h1 - h0) * (w1 - w0));
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc[j] *= inv;
+    store_vec<T, V>(y + pix * a.y_ld + c, acc);
+  }
+}
+
+template <typename T, int V>
+__global__ void bn_act_kernel(const EltArgs a) {
+  const int cg = a.C / V;
+  const long long total = (long long)a.N * a.HW * cg;
+  const T* x = static_cast<const T*>(a.x);
+  T* y = static_cast<T*>(a.y);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % cg) * V;
+    const long long pix = i / cg;
+    float f[V];
+    load_vec<T, V>(x + pix * a.x_ld + c, f);
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      float v = f[j];
+      if (a.scale) v = fmaf(v, __ldg(a.scale + c + j), __ldg(a.shift + c + j));
+      if (a.relu) v = fmaxf(v, 0.f);
+      f[j] = v;
+    }
+    store_vec<T, V>(y + pix * a.y_ld + c, f);
+  }
+}
+
+// NHWC (ld) -> NCHW through a 32x32 shared-memory tile: coalesced on both sides.
+template <typename T>
+__global__ void pack_output_kernel(const T* __restrict__ x, int HW, int C, int x_ld, T* __restrict__ y) {
+  __shared__ T tile[32][33];
+  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const long long n = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int p = p0 + ty + 8 * i, c = c0 + tx;
+    if (p < HW && c < C) tile[ty + 8 * i][tx] = x[(n * HW + p) * x_ld + c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + ty + 8 * i, p = p0 + tx;
+    if (p < HW && c < C) y[(n * C + c) * HW + p] = tile[tx][ty + 8 * i];
+  }
+}
+
+inline int grid_for(long long total, int block) {
+  long long g = (total + block - 1) / block;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g > 0 ? g : 1);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int is_bf16, cudaStream_t st) {
+  const long long total = (long long)N * H * W;
+  pack_input_kernel<<<grid_for(total, 256), 256, 0, st>>>(img, y, N, H * W, is_bf16);
+  return cudaGetLastError();
+}
+
+cudaError_t pool_launch(const PoolArgs& a, int is_bf16, cudaStream_t st) {
+  const long long pix = (long long)a.N * a.OH * a.OW;
+  if (is_bf16) {
+    if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
+      pool_kernel<__nv_bfloat16, 8><<<grid_for(pix * (a.C / 8), 256), 256, 0, st>>>(a);
+    else
+      pool_kernel<__nv_bfloat16, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+  } else {
+    if (a.C % 4 == 0 && a.x_ld % 4 == 0 && a.y_ld % 4 == 0 && aligned16(a.x) && aligned16(a.y))
+      pool_kernel<float, 4><<<grid_for(pix * (a.C / 4), 256), 256, 0, st>>>(a);
+    else
+      pool_kernel<float, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t adaptive_avgpool_launch(const AdaptiveArgs& a, int is_bf16, cudaStream_t st) {
+  const long long pix = (long long)a.N * a.OH * a.OW;
+  if (is_bf16) {
+    if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
+      adaptive_kernel<__nv_bfloat16, 8><<<grid_for(pix * (a.C / 8), 256), 256, 0, st>>>(a);
+    else
+      adaptive_kernel<__nv_bfloat16, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+  } else {
+    if (a.C % 4 == 0 && a.x_ld % 4 == 0 && a.y_ld % 4 == 0 && aligned16(a.x) && aligned16(a.y))
+      adaptive_kernel<float, 4><<<grid_for(pix * (a.C / 4), 256), 256, 0, st>>>(a);
+    else
+      adaptive_kernel<float, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t bn_act_launch(const EltArgs& a, int is_bf16, cudaStream_t st) {
+  const long long pix = (long long)a.N * a.HW;
+  if (is_bf16) {
+    if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
+      bn_act_kernel<__nv_bfloat16, 8><<<grid_for(pix * (a.C / 8), 256), 256, 0, st>>>(a);
+    else
+      bn_act_kernel<__nv_bfloat16, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+  } else {
+    if (a.C % 4 == 0 && a.x_ld % 4 == 0 && a.y_ld % 4 == 0 && aligned16(a.x) && aligned16(a.y))
+      bn_act_kernel<float, 4><<<grid_for(pix * (a.C / 4), 256), 256, 0, st>>>(a);
+    else
+      bn_act_kernel<float, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t pack_output_launch(const void* x, int N, int HW, int C, int x_ld, void* y, int is_bf16, cudaStream_t st) {
+  const size_t es = is_bf16 ? 2 : 4;
+  if (HW == 1) {  // NHWC == NCHW: a strided row copy
+    return cudaMemcpy2DAsync(y, C * es, x, (size_t)x_ld * es, C * es, N, cudaMemcpyDeviceToDevice, st);
+  }
+  dim3 grid((HW + 31) / 32, (C + 31) / 32, N), block(32, 8);
+  if (is_bf16)
+    pack_output_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(static_cast<const __nv_bfloat16*>(x), HW, C, x_ld,
+                                                             static_cast<__nv_bfloat16*>(y));
+  else
+    pack_output_kernel<float><<<grid, block, 0, st>>>(static_cast<const float*>(x), HW, C, x_ld, static_cast<float*>(y));
+  return cudaGetLastError();
+}
+
+}  // namespace hapi

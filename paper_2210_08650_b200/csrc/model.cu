@@ -1,0 +1,948 @@
+// Executor half of the C ABI: model creation (BN folding, weight packing, TMA
+// descriptors), split-aware launch plans (fusion never crosses the split boundary,
+// SURVEY.md 7.2 H3), the liveness-planned activation arena, and the launch loop of
+// hapi_prefix_forward ("executes the feature extraction part up to the split index",
+// PAPER.md:732; COS batch decoupled from the request, PAPER.md:732/740/750 -> chunking).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "arch.h"
+#include "common.h"
+#include "kernels.h"
+
+using namespace hapi;
+
+namespace hapi {
+
+namespace {
+thread_local std::string g_err;
+}
+
+hapi_status set_error(hapi_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+void clear_error() { g_err.clear(); }
+const char* last_error_cstr() { return g_err.c_str(); }
+
+}  // namespace hapi
+
+namespace {
+
+constexpr double BN_EPS = 1e-5;
+
+// ---------------------------------------------------------------- TMA encode (driver entry point)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// ---------------------------------------------------------------- model structures
+struct ConvW {
+  int cs = 0;        // channels per pixel consumed (stored)
+  int cout = 0, kh = 1, kw = 1, stride = 1, pad = 0;
+  int K = 0, Kp = 0;
+  void* w = nullptr;           // bf16 [Cout][Kp] (tc) or fp32 [K][Cout] (simt)
+  float* bias = nullptr;       // [Cout]
+  float* pro_scale = nullptr;  // [cs]
+  float* pro_shift = nullptr;
+  CUtensorMap tmap;
+  int bn = 0, mode = 0;
+  double real_flops_per_px = 0;  // 2 * K_real * Cout
+};
+
+enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT };
+
+struct View {
+  int buf = -1;       // -1: external (caller out, or caller images for PACK_IN input)
+  int C = 0, H = 0, W = 0, ld = 0, coff = 0;
+};
+
+struct Op {
+  OpType t;
+  View in, out, res;
+  bool has_res = false, relu = false, nchw_out = false, relu_in = false;
+  int conv = -1;
+  int pk = 0, ps = 0, pp = 0, pmode = 0;
+  const float* scale = nullptr;  // bn_act (device)
+  const float* shift = nullptr;
+  uint32_t kind = 0;             // plan_info kernel class
+  double flops = 0, bytes = 0;   // per image
+};
+
+struct Buf {
+  int64_t per_img = 0;  // bytes per image
+  int first = -1, last = -1;
+  int64_t offset = 0;   // per-image-scaled offset is not used; absolute offset for max_batch
+};
+
+struct Plan {
+  int split = 0;
+  std::vector<Op> ops;
+  std::vector<Buf> bufs;
+  int64_t arena_bytes = 0;
+  int64_t out_bytes_per_img = 0;
+};
+
+}  // namespace
+
+struct hapi_model {
+  hapi_model_desc d;
+  const ArchDesc* arch = nullptr;
+  bool bf16 = true;
+  int es = 2;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+  std::vector<ConvW> convs;
+  std::map<std::string, int> conv_index;
+  std::vector<const float*> host_params;  // valid during create only
+  std::vector<void*> allocs;
+  int64_t weight_bytes = 0;
+  std::vector<Plan> plans;  // index split - min_split
+  void* arena = nullptr;
+  int64_t arena_bytes = 0;
+  // host pipeline (lazy)
+  cudaStream_t copy_stream = nullptr;
+  void* stage_in[2] = {nullptr, nullptr};
+  void* stage_out[2] = {nullptr, nullptr};
+  int64_t stage_out_bytes = 0;
+  cudaEvent_t ev[8] = {};
+  bool host_ready = false;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+hapi_status dev_alloc(hapi_model* m, size_t bytes, void** p, bool weights) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess)
+    return set_error(e == cudaErrorMemoryAllocation ? HAPI_ERR_OUT_OF_MEMORY : HAPI_ERR_CUDA, "cudaMalloc(%zu): %s", bytes,
+                     cudaGetErrorString(e));
+  m->allocs.push_back(*p);
+  if (weights) m->weight_bytes += (int64_t)bytes;
+  return HAPI_OK;
+}
+
+template <typename T>
+hapi_status upload(hapi_model* m, const std::vector<T>& h, T** dptr) {
+  void* p;
+  hapi_status st = dev_alloc(m, h.size() * sizeof(T), &p, true);
+  if (st != HAPI_OK) return st;
+  cudaError_t e = cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_error(HAPI_ERR_CUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+  *dptr = static_cast<T*>(p);
+  return HAPI_OK;
+}
+
+uint16_t f2bf(float f) {  // round-to-nearest-even
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return (uint16_t)(u >> 16) | ((u & 0xffff) ? 0x40 : 0);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+const float* P(hapi_model* m, const std::string& name, int64_t expect_numel) {
+  int i = m->arch->find_param(name);
+  if (i < 0) return nullptr;
+  if (m->arch->params[i].numel() != expect_numel) return nullptr;
+  return m->host_params[i];
+}
+
+// BN eval as y = x*scale + shift (fp64)
+bool bn_affine(hapi_model* m, const std::string& bn, int c, std::vector<double>& scale, std::vector<double>& shift) {
+  const float* g = P(m, bn + ".weight", c);
+  const float* b = P(m, bn + ".bias", c);
+  const float* mu = P(m, bn + ".running_mean", c);
+  const float* var = P(m, bn + ".running_var", c);
+  if (!g || !b || !mu || !var) return false;
+  scale.resize(c);
+  shift.resize(c);
+  for (int i = 0; i < c; ++i) {
+    scale[i] = (double)g[i] / std::sqrt((double)var[i] + BN_EPS);
+    shift[i] = (double)b[i] - (double)mu[i] * scale[i];
+  }
+  return true;
+}
+
+struct ConvSpec {
+  std::string wname, bname, fold_bn, pro_bn;
+  int cin = 0, cout = 0, k = 1, stride = 1, pad = 0;
+  int cs = 0;            // stored channels per pixel of the input view (4 for the bf16 stem)
+  int fh = 0, fw = 0;    // linear on a flattened (cin/(fh*fw), fh, fw) map: permute columns
+  bool linear = false;
+};
+
+hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
+  std::string key = s.wname + "|" + s.bname + "|" + s.fold_bn + "|" + s.pro_bn + "|" + std::to_string(s.cs) + "|" +
+                    std::to_string(s.fh) + "x" + std::to_string(s.fw);
+  auto it = m->conv_index.find(key);
+  if (it != m->conv_index.end()) {
+    *out_idx = it->second;
+    return HAPI_OK;
+  }
+  const int kk = s.linear ? 1 : s.k;
+  const int64_t wn = (int64_t)s.cout * s.cin * kk * kk;
+  const float* w = P(m, s.wname, wn);
+  if (!w) return set_error(HAPI_ERR_INVALID_MODEL, "param %s missing or wrong shape", s.wname.c_str());
+  const float* b0 = nullptr;
+  if (!s.bname.empty() && !(b0 = P(m, s.bname, s.cout)))
+    return set_error(HAPI_ERR_INVALID_MODEL, "param %s missing", s.bname.c_str());
+  std::vector<double> fs, fb;
+  if (!s.fold_bn.empty() && !bn_affine(m, s.fold_bn, s.cout, fs, fb))
+    return set_error(HAPI_ERR_INVALID_MODEL, "bn %s missing", s.fold_bn.c_str());
+
+  ConvW cw;
+  cw.cs = s.cs;
+  cw.cout = s.cout;
+  cw.kh = cw.kw = kk;
+  cw.stride = s.stride;
+  cw.pad = s.pad;
+  cw.K = kk * kk * s.cs;
+  cw.real_flops_per_px = 2.0 * (double)kk * kk * s.cin * s.cout;
+  // element (o, k) of the GEMM B operand, k ordered (r, s, c) over the stored input channels
+  auto wval = [&](int o, int r, int t, int c) -> double {
+    if (c >= s.cin) return 0.0;  // padded stored channel
+    double v;
+    if (s.linear) {
+      // torchvision flattens NCHW: column c*fh*fw + h*fw + w; our input is NHWC-flattened
+      const int hw = s.fh * s.fw;
+      const int cf = s.cin / hw;
+      const int pix = c / cf, ch = c % cf;
+      v = w[(int64_t)o * s.cin + (int64_t)ch * hw + pix];
+    } else {
+      v = w[(((int64_t)o * s.cin + c) * kk + r) * kk + t];
+    }
+    if (!fs.empty()) v *= fs[o];
+    return v;
+  };
+  std::vector<float> bias(s.cout, 0.f);
+  bool has_bias = b0 || !fs.empty();
+  for (int o = 0; o < s.cout; ++o) {
+    double bv = b0 ? (double)b0[o] : 0.0;
+    if (!fs.empty()) bv = bv * fs[o] + fb[o];
+    bias[o] = (float)bv;
+  }
+  const int taps = kk * kk;
+  if (m->bf16) {
+    cw.Kp = (cw.K + 7) / 8 * 8;
+    std::vector<uint16_t> hw((size_t)s.cout * cw.Kp, 0);
+    for (int o = 0; o < s.cout; ++o)
+      for (int tap = 0; tap < taps; ++tap)
+        for (int c = 0; c < s.cs; ++c)
+          hw[(size_t)o * cw.Kp + tap * s.cs + c] = f2bf((float)wval(o, tap / kk, tap % kk, c));
+    uint16_t* dw;
+    hapi_status st = upload(m, hw, &dw);
+    if (st != HAPI_OK) return st;
+    cw.w = dw;
+    cw.bn = conv_tc_pick_bn(s.cout);
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)cw.Kp, (cuuint64_t)s.cout};
+    cuuint64_t strides[1] = {(cuuint64_t)cw.Kp * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)cw.bn};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&cw.tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cw.w, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for %s", (int)r, s.wname.c_str());
+  } else {
+    cw.Kp = cw.K;
+    std::vector<float> hw((size_t)cw.K * s.cout, 0.f);
+    for (int o = 0; o < s.cout; ++o)
+      for (int tap = 0; tap < taps; ++tap)
+        for (int c = 0; c < s.cs; ++c)
+          hw[(size_t)(tap * s.cs + c) * s.cout + o] = (float)wval(o, tap / kk, tap % kk, c);
+    float* dw;
+    hapi_status st = upload(m, hw, &dw);
+    if (st != HAPI_OK) return st;
+    cw.w = dw;
+  }
+  if (has_bias) {
+    hapi_status st = upload(m, bias, &cw.bias);
+    if (st != HAPI_OK) return st;
+  }
+  if (!s.pro_bn.empty()) {
+    std::vector<double> ps, ph;
+    if (!bn_affine(m, s.pro_bn, s.cin, ps, ph)) return set_error(HAPI_ERR_INVALID_MODEL, "bn %s missing", s.pro_bn.c_str());
+    std::vector<float> fps(ps.begin(), ps.end()), fph(ph.begin(), ph.end());
+    hapi_status st = upload(m, fps, &cw.pro_scale);
+    if (st == HAPI_OK) st = upload(m, fph, &cw.pro_shift);
+    if (st != HAPI_OK) return st;
+    cw.mode = 2;
+  } else {
+    cw.mode = (s.cs == 4 && m->bf16) ? 1 : 0;
+  }
+  if (m->bf16 && cw.mode != 1 && s.cs % 8 != 0)
+    return set_error(HAPI_ERR_UNSUPPORTED, "tensor-core conv needs C %% 8 == 0 (%s, C=%d)", s.wname.c_str(), s.cs);
+  m->convs.push_back(cw);
+  *out_idx = (int)m->convs.size() - 1;
+  m->conv_index[key] = *out_idx;
+  return HAPI_OK;
+}
+
+// ---------------------------------------------------------------- plan builder
+struct Builder {
+  hapi_model* m;
+  Plan p;
+  int new_buf(int64_t per_img_bytes) {
+    Buf b;
+    b.per_img = per_img_bytes;
+    p.bufs.push_back(b);
+    return (int)p.bufs.size() - 1;
+  }
+  View compact(int C, int H, int W) {
+    View v;
+    v.buf = new_buf((int64_t)C * H * W * m->es);
+    v.C = C; v.H = H; v.W = W; v.ld = C; v.coff = 0;
+    return v;
+  }
+  Op& emit(Op o) {
+    p.ops.push_back(o);
+    return p.ops.back();
+  }
+  hapi_status conv(const ConvSpec& cs, const View& in, const View& out, bool relu, const View* res, Op** op_out = nullptr) {
+    int ci;
+    hapi_status st = make_conv(m, cs, &ci);
+    if (st != HAPI_OK) return st;
+    Op o;
+    o.t = OP_CONV;
+    o.in = in; o.out = out; o.conv = ci; o.relu = relu;
+    if (res) { o.res = *res; o.has_res = true; }
+    o.kind = m->bf16 ? 0 : 1;
+    const ConvW& w = m->convs[ci];
+    const double px = (double)out.H * out.W;
+    o.flops = w.real_flops_per_px * px;
+    o.bytes = ((double)in.H * in.W * (cs.linear ? in.C : cs.cin) + px * w.cout * (res ? 2 : 1)) * m->es;
+    emit(o);
+    if (op_out) *op_out = &p.ops.back();
+    return HAPI_OK;
+  }
+  void pool(const View& in, const View& out, int k, int s, int pad, int mode) {
+    Op o;
+    o.t = OP_POOL;
+    o.in = in; o.out = out; o.pk = k; o.ps = s; o.pp = pad; o.pmode = mode;
+    o.kind = 2;
+    o.bytes = ((double)in.H * in.W * in.C + (double)out.H * out.W * out.C) * m->es;
+    emit(o);
+  }
+};
+
+bool is_fresh_output(const Plan& p, int buf) {
+  // buf written by the last op only and read by nobody
+  int refs = 0;
+  for (const Op& o : p.ops) {
+    if (o.in.buf == buf && o.t != OP_PACK_IN) ++refs;
+    if (o.has_res && o.res.buf == buf) ++refs;
+    if (o.out.buf == buf) ++refs;
+  }
+  return refs == 1 && !p.ops.empty() && p.ops.back().out.buf == buf;
+}
+
+hapi_status build_plan(hapi_model* m, int split, Plan* out) {
+  Builder b{m};
+  b.p.split = split;
+  const ArchDesc& A = *m->arch;
+  const int H0 = (int)m->d.in_h, W0 = (int)m->d.in_w;
+  const int cs0 = m->bf16 ? 4 : 3;
+  // a1: pack the caller's NCHW fp32 images
+  View cur = b.compact(cs0, H0, W0);
+  {
+    Op o;
+    o.t = OP_PACK_IN;
+    o.out = cur;
+    o.kind = 3;
+    o.bytes = (double)H0 * W0 * (3 * 4 + cs0 * m->es);
+    b.emit(o);
+  }
+  const auto& mods = A.mods;
+  int i = 0;
+  hapi_status st;
+  while (i < split) {
+    const ModDesc& md = mods[i];
+    switch (md.kind) {
+      case MK_CONV: {
+        const bool fold = i + 1 < split && mods[i + 1].kind == MK_BN;
+        const int j = i + 1 + (fold ? 1 : 0);
+        const bool relu = j < split && mods[j].kind == MK_RELU;
+        ConvSpec cs;
+        cs.wname = md.name + ".weight";
+        cs.bname = md.bias ? md.name + ".bias" : "";
+        cs.fold_bn = fold ? mods[i + 1].name : "";
+        cs.cin = md.cin; cs.cout = md.cout; cs.k = md.k; cs.stride = md.stride; cs.pad = md.pad;
+        cs.cs = cur.C;
+        View o = b.compact(md.cout, out_dim(cur.H, md.k, md.stride, md.pad), out_dim(cur.W, md.k, md.stride, md.pad));
+        if ((st = b.conv(cs, cur, o, relu, nullptr)) != HAPI_OK) return st;
+        cur = o;
+        i = j + (relu ? 1 : 0);
+        break;
+      }
+      case MK_BN: {
+        if (i + 2 < split && mods[i + 1].kind == MK_RELU && mods[i + 2].kind == MK_CONV) {
+          // DenseNet transition norm -> relu -> conv: bn-relu prologue on the conv's A operand
+          const ModDesc& cv = mods[i + 2];
+          ConvSpec cs;
+          cs.wname = cv.name + ".weight";
+          cs.pro_bn = md.name;
+          cs.cin = cv.cin; cs.cout = cv.cout; cs.k = cv.k; cs.stride = cv.stride; cs.pad = cv.pad;
+          cs.cs = cur.C;
+          View o = b.compact(cv.cout, out_dim(cur.H, cv.k, cv.stride, cv.pad), out_dim(cur.W, cv.k, cv.stride, cv.pad));
+          if ((st = b.conv(cs, cur, o, false, nullptr)) != HAPI_OK) return st;
+          cur = o;
+          i += 3;
+        } else {
+          const bool relu = i + 1 < split && mods[i + 1].kind == MK_RELU;
+          std::vector<double> sc, sh;
+          if (!bn_affine(m, md.name, md.cin, sc, sh)) return set_error(HAPI_ERR_INVALID_MODEL, "bn %s", md.name.c_str());
+          std::vector<float> fsc(sc.begin(), sc.end()), fsh(sh.begin(), sh.end());
+          float *dsc, *dsh;
+          if ((st = upload(m, fsc, &dsc)) != HAPI_OK || (st = upload(m, fsh, &dsh)) != HAPI_OK) return st;
+          View o = b.compact(cur.C, cur.H, cur.W);
+          Op op;
+          op.t = OP_BNACT;
+          op.in = cur; op.out = o; op.scale = dsc; op.shift = dsh; op.relu = relu;
+          op.kind = 4;
+          op.bytes = 2.0 * cur.C * cur.H * cur.W * m->es;
+          b.emit(op);
+          cur = o;
+          i += 1 + (relu ? 1 : 0);
+        }
+        break;
+      }
+      case MK_RELU: {
+        View o = b.compact(cur.C, cur.H, cur.W);
+        Op op;
+        op.t = OP_BNACT;
+        op.in = cur; op.out = o; op.relu = true;
+        op.kind = 4;
+        op.bytes = 2.0 * cur.C * cur.H * cur.W * m->es;
+        b.emit(op);
+        cur = o;
+        i += 1;
+        break;
+      }
+      case MK_MAXPOOL:
+      case MK_AVGPOOL: {
+        View o = b.compact(cur.C, out_dim(cur.H, md.k, md.stride, md.pad), out_dim(cur.W, md.k, md.stride, md.pad));
+        b.pool(cur, o, md.k, md.stride, md.pad, md.kind == MK_MAXPOOL ? 0 : 1);
+        cur = o;
+        i += 1;
+        break;
+      }
+      case MK_ADAPTIVE: {
+        if (!(cur.H == md.oh && cur.W == md.ow)) {
+          View o = b.compact(cur.C, md.oh, md.ow);
+          Op op;
+          op.t = OP_ADAPTIVE;
+          op.in = cur; op.out = o;
+          op.kind = 2;
+          op.bytes = ((double)cur.C * cur.H * cur.W + (double)cur.C * md.oh * md.ow) * m->es;
+          b.emit(op);
+          cur = o;
+        }
+        i += 1;
+        break;
+      }
+      case MK_DROPOUT:
+        i += 1;  // identity; flatten is a view
+        break;
+      case MK_LINEAR:
+      case MK_DENSE_CLS: {
+        if (md.kind == MK_DENSE_CLS) {
+          View o = b.compact(cur.C, 1, 1);
+          Op op;
+          op.t = OP_ADAPTIVE;
+          op.in = cur; op.out = o; op.relu_in = true;
+          op.kind = 2;
+          op.bytes = ((double)cur.C * cur.H * cur.W + cur.C) * m->es;
+          b.emit(op);
+          cur = o;
+        }
+        if (cur.ld != cur.C || cur.coff != 0) return set_error(HAPI_ERR_UNSUPPORTED, "linear on a strided view");
+        const bool relu = md.kind == MK_LINEAR && i + 1 < split && mods[i + 1].kind == MK_RELU;
+        ConvSpec cs;
+        cs.wname = md.name + ".weight";
+        cs.bname = md.name + ".bias";
+        cs.cin = md.cin; cs.cout = md.cout; cs.k = 1;
+        cs.linear = true;
+        cs.fh = cur.H; cs.fw = cur.W;
+        cs.cs = cur.C * cur.H * cur.W;
+        if (cs.cs != md.cin) return set_error(HAPI_ERR_INVALID_MODEL, "linear %s input %d != %d", md.name.c_str(), cs.cs, md.cin);
+        View in = cur;
+        in.C = cs.cs; in.H = 1; in.W = 1; in.ld = cs.cs;
+        View o = b.compact(md.cout, 1, 1);
+        if ((st = b.conv(cs, in, o, relu, nullptr)) != HAPI_OK) return st;
+        cur = o;
+        i += 1 + (relu ? 1 : 0);
+        break;
+      }
+      case MK_BASIC:
+      case MK_BOTTLENECK: {
+        const std::string& p = md.name;
+        const int OH = out_dim(cur.H, 3, md.stride, 1), OW = out_dim(cur.W, 3, md.stride, 1);
+        View x = cur;
+        View t;
+        if (md.kind == MK_BOTTLENECK) {
+          View t1 = b.compact(md.planes, cur.H, cur.W);
+          ConvSpec c1;
+          c1.wname = p + ".conv1.weight"; c1.fold_bn = p + ".bn1";
+          c1.cin = md.cin; c1.cout = md.planes; c1.k = 1; c1.cs = x.C;
+          if ((st = b.conv(c1, x, t1, true, nullptr)) != HAPI_OK) return st;
+          t = b.compact(md.planes, OH, OW);
+          ConvSpec c2;
+          c2.wname = p + ".conv2.weight"; c2.fold_bn = p + ".bn2";
+          c2.cin = md.planes; c2.cout = md.planes; c2.k = 3; c2.stride = md.stride; c2.pad = 1; c2.cs = md.planes;
+          if ((st = b.conv(c2, t1, t, true, nullptr)) != HAPI_OK) return st;
+        } else {
+          t = b.compact(md.planes, OH, OW);
+          ConvSpec c1;
+          c1.wname = p + ".conv1.weight"; c1.fold_bn = p + ".bn1";
+          c1.cin = md.cin; c1.cout = md.planes; c1.k = 3; c1.stride = md.stride; c1.pad = 1; c1.cs = x.C;
+          if ((st = b.conv(c1, x, t, true, nullptr)) != HAPI_OK) return st;
+        }
+        View idn = x;
+        if (md.ds) {
+          idn = b.compact(md.cout, OH, OW);
+          ConvSpec cd;
+          cd.wname = p + ".downsample.0.weight"; cd.fold_bn = p + ".downsample.1";
+          cd.cin = md.cin; cd.cout = md.cout; cd.k = 1; cd.stride = md.stride; cd.cs = x.C;
+          if ((st = b.conv(cd, x, idn, false, nullptr)) != HAPI_OK) return st;
+        }
+        ConvSpec cl;
+        if (md.kind == MK_BOTTLENECK) {
+          cl.wname = p + ".conv3.weight"; cl.fold_bn = p + ".bn3";
+          cl.cin = md.planes; cl.cout = md.cout; cl.k = 1; cl.cs = md.planes;
+        } else {
+          cl.wname = p + ".conv2.weight"; cl.fold_bn = p + ".bn2";
+          cl.cin = md.planes; cl.cout = md.cout; cl.k = 3; cl.pad = 1; cl.cs = md.planes;
+        }
+        // out = relu(bn(conv(t)) + idn), written in place over idn
+        if ((st = b.conv(cl, t, idn, true, &idn)) != HAPI_OK) return st;
+        cur = idn;
+        i += 1;
+        break;
+      }
+      case MK_DENSEBLOCK: {
+        const int C0 = md.cin, Ct = md.cout;
+        View blk = b.compact(Ct, cur.H, cur.W);
+        View head = blk;
+        head.C = C0;
+        if (cur.buf >= 0 && is_fresh_output(b.p, cur.buf) && cur.ld == cur.C && cur.coff == 0) {
+          // retarget the producing op (pool0 / transition pool) into the block buffer
+          b.p.ops.back().out = head;
+          b.p.bufs[cur.buf].per_img = 0;
+        } else {
+          Op op;
+          op.t = OP_BNACT;
+          op.in = cur; op.out = head;
+          op.kind = 4;
+          op.bytes = 2.0 * C0 * cur.H * cur.W * m->es;
+          b.emit(op);
+        }
+        View tmid = b.compact(md.bn_size * md.growth, cur.H, cur.W);
+        for (int j = 0; j < md.nlayers; ++j) {
+          const std::string q = md.name + ".denselayer" + std::to_string(j + 1);
+          const int cj = C0 + md.growth * j;
+          View in = blk;
+          in.C = cj;
+          ConvSpec c1;
+          c1.wname = q + ".conv1.weight"; c1.pro_bn = q + ".norm1"; c1.fold_bn = q + ".norm2";
+          c1.cin = cj; c1.cout = md.bn_size * md.growth; c1.k = 1; c1.cs = cj;
+          if ((st = b.conv(c1, in, tmid, true, nullptr)) != HAPI_OK) return st;
+          View o = blk;
+          o.C = md.growth;
+          o.coff = cj;
+          ConvSpec c2;
+          c2.wname = q + ".conv2.weight";
+          c2.cin = md.bn_size * md.growth; c2.cout = md.growth; c2.k = 3; c2.pad = 1; c2.cs = md.bn_size * md.growth;
+          if ((st = b.conv(c2, tmid, o, false, nullptr)) != HAPI_OK) return st;
+        }
+        cur = blk;
+        i += 1;
+        break;
+      }
+    }
+  }
+
+  // a7: deliver layer `split` into the caller's buffer as contiguous NCHW.
+  Plan& p = b.p;
+  b.p.out_bytes_per_img = (int64_t)cur.C * cur.H * cur.W * m->es;
+  Op& last = p.ops.back();
+  const bool compact = cur.ld == cur.C && cur.coff == 0;
+  const bool same_view = cur.buf >= 0 && last.out.buf == cur.buf && last.out.C == cur.C && last.out.ld == cur.ld &&
+                         last.out.coff == cur.coff;
+  const bool can_direct = same_view && compact && last.t != OP_PACK_IN;
+  if (can_direct && last.t == OP_CONV) {
+    last.out.buf = -1;
+    last.nchw_out = true;
+  } else if (can_direct && cur.H == 1 && cur.W == 1 && (last.t == OP_POOL || last.t == OP_ADAPTIVE || last.t == OP_BNACT)) {
+    last.out.buf = -1;
+  } else {
+    Op op;
+    op.t = OP_PACK_OUT;
+    op.in = cur;
+    op.out.buf = -1;
+    op.kind = 3;
+    op.bytes = 2.0 * cur.C * cur.H * cur.W * m->es;
+    b.emit(op);
+  }
+  // liveness + first-fit arena placement (sizes at max_batch)
+  for (size_t k = 0; k < p.ops.size(); ++k) {
+    const Op& o = p.ops[k];
+    auto touch = [&](int buf) {
+      if (buf < 0) return;
+      Buf& bb = p.bufs[buf];
+      if (bb.first < 0) bb.first = (int)k;
+      bb.last = (int)k;
+    };
+    if (o.t != OP_PACK_IN) touch(o.in.buf);
+    if (o.has_res) touch(o.res.buf);
+    touch(o.out.buf);
+  }
+  const int64_t B = m->d.max_batch;
+  std::vector<int> order;
+  for (size_t k = 0; k < p.bufs.size(); ++k)
+    if (p.bufs[k].first >= 0 && p.bufs[k].per_img > 0) order.push_back((int)k);
+  std::sort(order.begin(), order.end(), [&](int a, int c) { return p.bufs[a].per_img * B > p.bufs[c].per_img * B; });
+  std::vector<int> placed;
+  int64_t top = 0;
+  for (int id : order) {
+    Buf& bb = p.bufs[id];
+    const int64_t sz = (bb.per_img * B + 255) / 256 * 256;
+    // candidate offsets: 0 and the end of every overlapping placed buffer
+    std::vector<int64_t> cands{0};
+    for (int q : placed) {
+      const Buf& o = p.bufs[q];
+      if (o.last < bb.first || o.first > bb.last) continue;
+      cands.push_back(o.offset + (o.per_img * B + 255) / 256 * 256);
+    }
+    std::sort(cands.begin(), cands.end());
+    for (int64_t off : cands) {
+      bool ok = true;
+      for (int q : placed) {
+        const Buf& o = p.bufs[q];
+        if (o.last < bb.first || o.first > bb.last) continue;
+        const int64_t oe = o.offset + (o.per_img * B + 255) / 256 * 256;
+        if (off < oe && o.offset < off + sz) { ok = false; break; }
+      }
+      if (ok) { bb.offset = off; break; }
+    }
+    placed.push_back(id);
+    top = std::max(top, bb.offset + sz);
+  }
+  p.arena_bytes = top;
+  *out = std::move(b.p);
+  return HAPI_OK;
+}
+
+// ---------------------------------------------------------------- launching
+inline char* vptr(hapi_model* m, const Plan& p, const View& v, void* ext) {
+  char* base = v.buf < 0 ? static_cast<char*>(ext) : static_cast<char*>(m->arena) + p.bufs[v.buf].offset;
+  return base + (int64_t)v.coff * m->es;
+}
+
+hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const float* images, void* out, cudaStream_t st) {
+  cudaError_t e = cudaSuccess;
+  const int isb = m->bf16 ? 1 : 0;
+  switch (o.t) {
+    case OP_PACK_IN:
+      e = pack_input_launch(images, vptr(m, p, o.out, out), nb, o.out.H, o.out.W, isb, st);
+      break;
+    case OP_CONV: {
+      const ConvW& w = m->convs[o.conv];
+      ConvArgs a;
+      a.x = vptr(m, p, o.in, out);
+      a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = w.cs; a.x_ld = o.in.ld;
+      a.KH = w.kh; a.KW = w.kw; a.stride = w.stride; a.pad = w.pad;
+      a.OH = o.out.H; a.OW = o.out.W;
+      a.Cout = w.cout;
+      a.K = w.K;
+      a.w = w.w;
+      a.bias = w.bias;
+      a.pro_scale = w.pro_scale;
+      a.pro_shift = w.pro_shift;
+      a.res = o.has_res ? vptr(m, p, o.res, out) : nullptr;
+      a.res_ld = o.has_res ? o.res.ld : 0;
+      a.y = vptr(m, p, o.out, out);
+      a.y_ld = o.out.ld;
+      a.relu = o.relu;
+      a.nchw = o.nchw_out;
+      a.M = (long long)nb * a.OH * a.OW;
+      e = m->bf16 ? conv_tc_launch(a, &w.tmap, w.bn, w.mode, m->num_sms, st) : conv_simt_launch(a, st);
+      break;
+    }
+    case OP_POOL: {
+      PoolArgs a;
+      a.x = vptr(m, p, o.in, out);
+      a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = o.in.C; a.x_ld = o.in.ld;
+      a.y = vptr(m, p, o.out, out);
+      a.OH = o.out.H; a.OW = o.out.W; a.y_ld = o.out.buf < 0 ? o.out.C : o.out.ld;
+      a.k = o.pk; a.stride = o.ps; a.pad = o.pp; a.mode = o.pmode;
+      e = pool_launch(a, isb, st);
+      break;
+    }
+    case OP_ADAPTIVE: {
+      AdaptiveArgs a;
+      a.x = vptr(m, p, o.in, out);
+      a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = o.in.C; a.x_ld = o.in.ld;
+      a.y = vptr(m, p, o.out, out);
+      a.OH = o.out.H; a.OW = o.out.W; a.y_ld = o.out.buf < 0 ? o.out.C : o.out.ld;
+      a.relu_in = o.relu_in;
+      e = adaptive_avgpool_launch(a, isb, st);
+      break;
+    }
+    case OP_BNACT: {
+      EltArgs a;
+      a.x = vptr(m, p, o.in, out);
+      a.N = nb; a.HW = o.in.H * o.in.W; a.C = o.in.C; a.x_ld = o.in.ld;
+      a.y = vptr(m, p, o.out, out);
+      a.y_ld = o.out.buf < 0 ? o.out.C : o.out.ld;
+      a.scale = o.scale; a.shift = o.shift; a.relu = o.relu;
+      e = bn_act_launch(a, isb, st);
+      break;
+    }
+    case OP_PACK_OUT:
+      e = pack_output_launch(vptr(m, p, o.in, out), nb, o.in.H * o.in.W, o.in.C, o.in.ld, out, isb, st);
+      break;
+  }
+  if (e != cudaSuccess) return set_error(HAPI_ERR_CUDA, "launch of op %d failed: %s", (int)o.t, cudaGetErrorString(e));
+  return HAPI_OK;
+}
+
+hapi_status run_chunk(hapi_model* m, const Plan& p, int nb, const float* images, void* out, cudaStream_t st,
+                      cudaEvent_t* evs = nullptr) {
+  for (size_t k = 0; k < p.ops.size(); ++k) {
+    if (evs) cudaEventRecord(evs[k], st);
+    hapi_status s = launch_op(m, p, p.ops[k], nb, images, out, st);
+    if (s != HAPI_OK) return s;
+  }
+  if (evs) cudaEventRecord(evs[p.ops.size()], st);
+  return HAPI_OK;
+}
+
+const Plan* get_plan(hapi_model* m, uint32_t split) {
+  if (split < m->d.min_split || split > m->d.max_split) return nullptr;
+  return &m->plans[split - m->d.min_split];
+}
+
+}  // namespace
+
+extern "C" {
+
+hapi_status hapi_model_create(const hapi_model_desc* desc, const float* const* params, uint32_t n_params, hapi_model** out) {
+  clear_error();
+  if (!desc || !out || (!params && n_params)) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  const ArchDesc* A = get_arch(desc->arch);
+  if (!A) return set_error(HAPI_ERR_INVALID_MODEL, "unknown arch %d", (int)desc->arch);
+  if (desc->act != HAPI_F32 && desc->act != HAPI_BF16) return set_error(HAPI_ERR_INVALID_ARGUMENT, "dtype");
+  const uint32_t L = (uint32_t)A->mods.size();
+  if (desc->min_split < 1 || desc->min_split > desc->max_split || desc->max_split > L)
+    return set_error(HAPI_ERR_INVALID_ARGUMENT, "split range [%u,%u] not within [1,%u]", desc->min_split, desc->max_split, L);
+  if (desc->max_batch < 1) return set_error(HAPI_ERR_INVALID_ARGUMENT, "max_batch = 0");
+  if (n_params != A->params.size())
+    return set_error(HAPI_ERR_INVALID_MODEL, "n_params %u != %zu", n_params, A->params.size());
+  for (uint32_t k = 0; k < n_params; ++k)
+    if (!params[k]) return set_error(HAPI_ERR_INVALID_ARGUMENT, "params[%u] is null", k);
+  // shape validity at this image size
+  {
+    Shape s{3, (int)desc->in_h, (int)desc->in_w, false};
+    for (uint32_t k = 0; k < desc->max_split; ++k) {
+      bool ok;
+      s = infer(A->mods[k], s, &ok);
+      if (!ok) return set_error(HAPI_ERR_INVALID_MODEL, "layer %s empty at %ux%u", A->mods[k].name.c_str(), desc->in_h, desc->in_w);
+    }
+  }
+  HAPI_CUDA_TRY(cudaSetDevice(desc->device));
+  std::unique_ptr<hapi_model> m(new hapi_model());
+  m->d = *desc;
+  m->arch = A;
+  m->bf16 = desc->act == HAPI_BF16;
+  m->es = m->bf16 ? 2 : 4;
+  HAPI_CUDA_TRY(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, desc->device));
+  if (m->bf16) {
+    int major = 0, minor = 0;
+    HAPI_CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, desc->device));
+    HAPI_CUDA_TRY(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, desc->device));
+    if (major != 10 || minor != 0)
+      return set_error(HAPI_ERR_UNSUPPORTED, "bf16 tcgen05 path is built for sm_100a; device is sm_%d%d", major, minor);
+  }
+  m->host_params.assign(params, params + n_params);
+  for (uint32_t s = desc->min_split; s <= desc->max_split; ++s) {
+    Plan p;
+    hapi_status st = build_plan(m.get(), (int)s, &p);
+    if (st != HAPI_OK) {
+      hapi_model_destroy(m.release());
+      return st;
+    }
+    m->arena_bytes = std::max(m->arena_bytes, p.arena_bytes);
+    m->plans.push_back(std::move(p));
+  }
+  m->host_params.clear();
+  {
+    hapi_status st = dev_alloc(m.get(), (size_t)m->arena_bytes, &m->arena, false);
+    if (st != HAPI_OK) {
+      hapi_model_destroy(m.release());
+      return st;
+    }
+  }
+  *out = m.release();
+  return HAPI_OK;
+}
+
+hapi_status hapi_model_set_stream(hapi_model* m, void* s) {
+  clear_error();
+  if (!m) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null model");
+  m->stream = static_cast<cudaStream_t>(s);
+  return HAPI_OK;
+}
+
+hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
+  clear_error();
+  if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
+  const Plan* p = get_plan(m, split_idx);
+  if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
+  HAPI_CUDA_TRY(cudaGetLastError());
+  const int64_t img_elems = 3ll * m->d.in_h * m->d.in_w;
+  for (uint64_t c0 = 0; c0 < batch; c0 += m->d.max_batch) {
+    const int nb = (int)std::min<uint64_t>(m->d.max_batch, batch - c0);
+    hapi_status st = run_chunk(m, *p, nb, images + c0 * img_elems, static_cast<char*>(out) + c0 * p->out_bytes_per_img, m->stream);
+    if (st != HAPI_OK) return st;
+  }
+  return HAPI_OK;
+}
+
+hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out,
+                                      float* ms, uint32_t cap) {
+  clear_error();
+  if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (batch == 0 || batch > m->d.max_batch) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch must be in [1, max_batch]");
+  const Plan* p = get_plan(m, split_idx);
+  if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
+  std::vector<cudaEvent_t> evs(p->ops.size() + 1);
+  for (auto& e : evs) HAPI_CUDA_TRY(cudaEventCreate(&e));
+  hapi_status st = run_chunk(m, *p, (int)batch, images, out, m->stream, evs.data());
+  if (st == HAPI_OK) {
+    cudaError_t e = cudaEventSynchronize(evs.back());
+    if (e != cudaSuccess) st = set_error(HAPI_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+  }
+  if (st == HAPI_OK && ms)
+    for (size_t k = 0; k < p->ops.size() && k < cap; ++k) cudaEventElapsedTime(&ms[k], evs[k], evs[k + 1]);
+  for (auto& e : evs) cudaEventDestroy(e);
+  return st;
+}
+
+hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
+  clear_error();
+  if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
+  const Plan* p = get_plan(m, split_idx);
+  if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
+  const int64_t img_bytes = 12ll * m->d.in_h * m->d.in_w;
+  int64_t max_out = 0;
+  for (const Plan& q : m->plans) max_out = std::max(max_out, q.out_bytes_per_img);
+  if (!m->host_ready) {
+    HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      hapi_status st = dev_alloc(m, (size_t)img_bytes * m->d.max_batch, &m->stage_in[k], false);
+      if (st == HAPI_OK) st = dev_alloc(m, (size_t)max_out * m->d.max_batch, &m->stage_out[k], false);
+      if (st != HAPI_OK) return st;
+    }
+    for (auto& e : m->ev) HAPI_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    m->host_ready = true;
+  }
+  // ev[0..1] h2d done, ev[2..3] compute done, ev[4..5] d2h done (slot reuse)
+  cudaStream_t cs = m->stream, xs = m->copy_stream;
+  const uint64_t B = m->d.max_batch;
+  const uint64_t nchunks = (batch + B - 1) / B;
+  for (uint64_t c = 0; c < nchunks; ++c) {
+    const int k = (int)(c & 1);
+    const uint64_t c0 = c * B;
+    const int nb = (int)std::min<uint64_t>(B, batch - c0);
+    if (c >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(xs, m->ev[2 + k], 0));  // stage_in[k] free once chunk c-2 computed
+    HAPI_CUDA_TRY(cudaMemcpyAsync(m->stage_in[k], reinterpret_cast<const char*>(images) + c0 * img_bytes,
+                                  (size_t)nb * img_bytes, cudaMemcpyHostToDevice, xs));
+    HAPI_CUDA_TRY(cudaEventRecord(m->ev[k], xs));
+    HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[k], 0));
+    if (c >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[4 + k], 0));  // stage_out[k] drained
+    hapi_status st = run_chunk(m, *p, nb, static_cast<const float*>(m->stage_in[k]), m->stage_out[k], cs);
+    if (st != HAPI_OK) return st;
+    HAPI_CUDA_TRY(cudaEventRecord(m->ev[2 + k], cs));
+    HAPI_CUDA_TRY(cudaStreamWaitEvent(xs, m->ev[2 + k], 0));
+    HAPI_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + c0 * p->out_bytes_per_img, m->stage_out[k],
+                                  (size_t)nb * p->out_bytes_per_img, cudaMemcpyDeviceToHost, xs));
+    HAPI_CUDA_TRY(cudaEventRecord(m->ev[4 + k], xs));
+  }
+  HAPI_CUDA_TRY(cudaStreamSynchronize(xs));
+  HAPI_CUDA_TRY(cudaStreamSynchronize(cs));
+  return HAPI_OK;
+}
+
+hapi_status hapi_model_device_bytes(const hapi_model* m, uint64_t* wb, uint64_t* ab) {
+  clear_error();
+  if (!m) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null model");
+  if (wb) *wb = (uint64_t)m->weight_bytes;
+  if (ab) *ab = (uint64_t)m->arena_bytes;
+  return HAPI_OK;
+}
+
+hapi_status hapi_plan_info(const hapi_model* m, uint32_t split_idx, uint32_t* n, uint32_t* kind, double* flops,
+                           double* bytes, uint32_t cap) {
+  clear_error();
+  if (!m || !n) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (split_idx < m->d.min_split || split_idx > m->d.max_split) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx");
+  const Plan& p = m->plans[split_idx - m->d.min_split];
+  *n = (uint32_t)p.ops.size();
+  for (size_t k = 0; k < p.ops.size() && k < cap; ++k) {
+    if (kind) kind[k] = p.ops[k].kind;
+    if (flops) flops[k] = p.ops[k].flops;
+    if (bytes) bytes[k] = p.ops[k].bytes;
+  }
+  return HAPI_OK;
+}
+
+void hapi_model_destroy(hapi_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->d.device);
+  if (m->host_ready) {
+    cudaStreamSynchronize(m->copy_stream);
+    for (auto& e : m->ev) cudaEventDestroy(e);
+    cudaStreamDestroy(m->copy_stream);
+  }
+  for (void* p : m->allocs) cudaFree(p);
+  delete m;
+}
+
+const char* hapi_last_error(void) { return last_error_cstr(); }
+
+const char* hapi_build_info(void) {
+  return "hapi-b200 (sm_100a tcgen05/TMEM/TMA implicit-GEMM conv; fp32 SIMT path); built " __DATE__ " " __TIME__;
+}
+
+}  // extern "C"
