@@ -1,0 +1,328 @@
+"""bench.py -- storage-side prefix-forward throughput of HAPI (arXiv 2210.08650) on B200.
+
+A "step" is one hapi_prefix_forward of one batch through layers 1..s (the whole hot path,
+SURVEY.md 8(a) rows a1-a8) on every GPU.  Default workload = BASELINE.json configs[2]:
+ResNet50 split at the paper's chosen index s=21 (Alg. 1 at Table 6's settings, DESIGN.md
+reading R9), batch 512 per GPU, bf16, synthetic 3x224x224 fp32 images (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl reference]
+  N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+Prints ONE JSON line on rank 0.  The oracle (oracle/) is executed only by the
+cpu_baseline leg and by --impl reference, never on the timed path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (arch, act, split, batch per GPU, image seed)
+    "resnet50_s21_b512": ("resnet50", "bf16", 21, 512, 3),
+    "resnet50_s20_b512": ("resnet50", "bf16", 20, 512, 3),
+    "resnet18_s10_b200": ("resnet18", "bf16", 10, 200, 2),
+    "alexnet_s13_b8_f32": ("alexnet", "f32", 13, 8, 1),
+    "densenet121_s9_b512": ("densenet121", "bf16", 9, 512, 5),
+    "densenet121_s20_b512": ("densenet121", "bf16", 20, 512, 5),
+    "vgg11_s21_b256": ("vgg11", "bf16", 21, 256, 4),
+}
+METRIC = "prefix-forward images/sec at split layer"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    src="measured", sm_max=d.get("sm_max_mhz"))
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)", sm_max=1965.0)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons, pw = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+def cpu_oracle_rate(arch, split, seed, n_img, h=224, w=224):
+    """The oracle as it stands (NumPy fp64), on the host cores; returns (img/s, seconds, threads)."""
+    import hapi_inputs
+    from oracle import prefix
+    P = hapi_inputs.params(arch, 1000 + seed)
+    x = hapi_inputs.images(n_img, seed, h, w)
+    t0 = time.perf_counter()
+    prefix.prefix_forward(arch, P, x, split)
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] or [1])
+    except Exception:  # noqa: BLE001
+        threads = len(os.sched_getaffinity(0))
+    return n_img / dt, dt, threads
+
+
+def cpu_model():
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return "unknown"
+
+
+def run_reference(args, wl):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    arch, act, split, batch, seed = WORKLOADS[wl]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_img = 1
+    for _ in range(args.warmup):
+        cpu_oracle_rate(arch, split, seed, n_img)
+        break  # one warm-up pass is enough for a NumPy program; more would exceed the time budget
+    times = []
+    for _ in range(args.steps):
+        _, dt, threads = cpu_oracle_rate(arch, split, seed, n_img)
+        times.append(dt)
+    tot = sum(times)
+    val = n_img * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "img/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(wl, args.gpus),
+        "cpu_baseline": {"value": val, "unit": "img/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{n_img} image(s) per step of {wl}, NumPy fp64 oracle, {cpu_model()}"},
+        "e2e": {"value": val, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_of(wl, n):
+    arch, act, split, batch, _ = WORKLOADS[wl]
+    return {"workload": wl, "split_idx": split, "batch_per_gpu": batch, "global_batch": batch * n,
+            "image": "3x224x224 fp32 NCHW, N(0,1)", "weights": "random-init (seeded), BN folded",
+            "l2": "inputs larger than L2 (batch x 602112 B per GPU)" if batch * 602112 > 126e6 else "L2 flushed between steps",
+            "parallelism": f"dp{n} (contiguous image shards, no data-path collective)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="resnet50_s21_b512", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="hapi", choices=["hapi", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = args.workload
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import hapi_inputs
+    import paper_2210_08650_b200 as H
+
+    arch, act, split, batch, seed = WORKLOADS[wl]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+
+    P = hapi_inputs.params(arch, 1000 + seed)
+    model = H.Model(arch, act, list(P.values()), batch, split, split, device=local)
+    stream = torch.cuda.current_stream()
+    model.set_stream(stream.cuda_stream)
+    # this rank's contiguous shard of images (weak scaling: batch per GPU fixed)
+    x_host = torch.from_numpy(hapi_inputs.images(batch, seed * 1000 + rank))
+    x = x_host.cuda()
+    es = 4 if act == "f32" else 2
+    out_numel = model.out_bytes[split - 1] // es * batch
+    out = torch.empty(out_numel, dtype=torch.float32 if act == "f32" else torch.bfloat16, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(args.warmup):
+        model.forward(split, x, out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            model.forward(split, x, out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    checksum = float(out.float().sum().item())
+    # max over ranks (NCCL all_gather of [count, elapsed_ns, checksum bits])
+    meta = torch.tensor([batch * args.steps, int(ms * 1e6), int(np.float64(checksum).view(np.int64))],
+                        dtype=torch.int64, device="cuda")
+    if world > 1:
+        allm = torch.empty(world * 3, dtype=torch.int64, device="cuda")
+        dist.all_gather_into_tensor(allm, meta)
+        allm = allm.view(world, 3).cpu().numpy()
+    else:
+        allm = meta.view(1, 3).cpu().numpy()
+    max_ms = allm[:, 1].max() / 1e6
+    total_imgs = int(allm[:, 0].sum())
+    value = total_imgs / (max_ms / 1e3)
+
+    # per-launch profile (separate pass with CUDA events between launches)
+    info = model.plan_info(split)
+    prof = np.zeros(info["n"])
+    reps = 3
+    for _ in range(reps):
+        prof += np.array(model.forward_timed(split, x, out))
+    prof /= reps
+    kinds = np.array(info["kind"])
+    flops = np.array(info["flops"]) * batch
+    byts = np.array(info["bytes"]) * batch
+    cls_time = {H.KERNEL_CLASSES[k]: float(prof[kinds == k].sum()) for k in set(info["kind"])}
+    dom = max(cls_time, key=cls_time.get)
+    dk = [k for k, v in H.KERNEL_CLASSES.items() if v == dom][0]
+    sel = kinds == dk
+    dom_ms = float(prof[sel].sum())
+    n_dom = int(sel.sum())
+    step_ms_prof = float(prof.sum())
+    if dom in ("conv_tc",):
+        achieved = flops[sel].sum() / (dom_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["bf16_sus"], "peak_kind": f"bf16 sustained ({peaks['src']})",
+                "frac_of_burst": achieved / peaks["bf16"]}
+    elif dom == "conv_simt":
+        # fp32 FFMA ALU peak: 148 SMs x 128 FP32 lanes x 2 FLOP x max clock
+        alu = 148 * 128 * 2 * (peaks["sm_max"] or 1965.0) * 1e6 / 1e12
+        achieved = flops[sel].sum() / (dom_ms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": alu, "unit": "TFLOP/s", "frac": achieved / alu,
+                "peak_kind": "fp32 FFMA: 148 SM x 128 lanes x 2 x sm_max_mhz (DESIGN.md)"}
+    else:
+        achieved = byts[sel].sum() / (dom_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm"], "peak_kind": f"HBM copy ({peaks['src']})"}
+    roof.update({"kernel": dom, "launches_per_step": n_dom, "share_of_step": dom_ms / step_ms_prof,
+                 "ms_per_launch": dom_ms / max(n_dom, 1), "traffic": None})
+    tr = os.path.join(ROOT, "profiles", f"traffic_{wl}.json")
+    if os.path.exists(tr):
+        roof["traffic"] = json.load(open(tr)).get("bytes_per_launch")
+    class_share = {k: v / step_ms_prof for k, v in cls_time.items()}
+
+    # end to end through the public C-ABI call with HOST buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        xp = x_host.pin_memory()
+        oh = torch.empty(out_numel, dtype=out.dtype).pin_memory()
+        model.forward_host(split, xp, oh)
+        barrier()
+        t0 = time.perf_counter()
+        ksteps = max(3, args.steps // 2)
+        for _ in range(ksteps):
+            model.forward_host(split, xp, oh)
+        dt = time.perf_counter() - t0
+        dts = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(dts, op=dist.ReduceOp.MAX)
+        e2e = {"value": batch * ksteps * world / float(dts.item()), "unit": "img/s",
+               "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_numel * es),
+               "steps": ksteps, "note": "hapi_prefix_forward_host: pinned H2D + forward + D2H, 2-stream pipelined"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, dt, threads = cpu_oracle_rate(arch, split, seed, 1)
+        n2 = max(1, min(8, int(15.0 / max(dt, 1e-3))))
+        if n2 > 1:
+            rate, dt, threads = cpu_oracle_rate(arch, split, seed, n2)
+        cpu = {"value": rate, "unit": "img/s", "cores": threads, "kind": "oracle",
+               "sample": f"{n2} image(s) of {wl} through the NumPy fp64 oracle in {dt:.1f}s on {cpu_model()}"}
+
+    if rank == 0:
+        fl_img = float(np.array(info["flops"]).sum())
+        line = {
+            "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": act, "data": "synthetic", "config": config_of(wl, world),
+            "pct_bf16_peak": {"flop_per_img": fl_img,
+                              "of_burst": value / world * fl_img / 1e12 / peaks["bf16"],
+                              "of_sustained": value / world * fl_img / 1e12 / peaks["bf16_sus"],
+                              "of_2.25PF_datasheet": value / world * fl_img / 1e12 / 2250.0},
+            "roofline": roof, "kernel_class_share": class_share, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "e2e": e2e, "gpu_launches": int(info["n"] - sum(1 for k in info["kind"] if k == 3 and False)) * args.steps,
+            "gpu_launches_per_step": int(info["n"]),
+            "checksum_ranks": [float(np.int64(v).view(np.float64)) for v in allm[:, 2]],
+        }
+        print(json.dumps(line), flush=True)
+    model.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

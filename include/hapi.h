@@ -174,6 +174,10 @@ HAPI_API hapi_status hapi_plan_info(const hapi_model *m, uint32_t split_idx, uin
                            uint32_t *kind, double *flops_per_img, double *bytes_per_img,
                            uint32_t cap);
 
+/* Human-readable description of launch `op` of split_idx's plan (kernel, shape, fusions),
+ * NUL-terminated into buf[cap].  Diagnostics only. */
+HAPI_API hapi_status hapi_plan_describe(const hapi_model *m, uint32_t split_idx, uint32_t op, char *buf, uint32_t cap);
+
 /* Same as hapi_prefix_forward on one chunk (batch <= max_batch), recording a CUDA event
  * before and after every launch; per-launch milliseconds are written to ms[i] (< cap)
  * after an internal stream synchronize.  Instrumentation for measurement only. */

@@ -157,7 +157,12 @@ class Model:
         fl = (C.c_double * n.value)()
         by = (C.c_double * n.value)()
         _check(_lib.hapi_plan_info(self._h, split_idx, C.byref(n), k, fl, by, n.value))
-        return dict(n=n.value, kind=list(k), flops=list(fl), bytes=list(by))
+        buf = C.create_string_buffer(256)
+        desc = []
+        for i in range(n.value):
+            _check(_lib.hapi_plan_describe(self._h, split_idx, i, buf, 256))
+            desc.append(buf.value.decode())
+        return dict(n=n.value, kind=list(k), flops=list(fl), bytes=list(by), desc=desc)
 
 
 KERNEL_CLASSES = {0: "conv_tc", 1: "conv_simt", 2: "pool", 3: "pack", 4: "eltwise"}

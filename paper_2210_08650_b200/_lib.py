@@ -10,7 +10,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libhapi.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2210_08650_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: run `python paper_2210_08650_b200/build.py` "
                       "(there is no CPU fallback for the HAPI prefix forward)")
 lib = C.CDLL(LIB_PATH)
 
@@ -56,11 +56,12 @@ hapi_model_device_bytes = _sig("hapi_model_device_bytes", C.c_int, C.c_void_p, P
 hapi_plan_info = _sig("hapi_plan_info", C.c_int, C.c_void_p, u32, P_u32, P_u32, P_dbl, P_dbl, u32)
 hapi_prefix_forward_timed = _sig("hapi_prefix_forward_timed", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p,
                                  P_f32, u32)
+hapi_plan_describe = _sig("hapi_plan_describe", C.c_int, C.c_void_p, u32, u32, C.c_char_p, u32)
 hapi_model_destroy = _sig("hapi_model_destroy", None, C.c_void_p)
 hapi_last_error = _sig("hapi_last_error", C.c_char_p)
 hapi_build_info = _sig("hapi_build_info", C.c_char_p)
 
 EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_choose_split", "hapi_num_params",
             "hapi_param_info", "hapi_model_create", "hapi_model_set_stream", "hapi_prefix_forward",
-            "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_prefix_forward_timed",
+            "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_plan_describe", "hapi_prefix_forward_timed",
             "hapi_model_destroy", "hapi_last_error", "hapi_build_info"]

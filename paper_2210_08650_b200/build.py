@@ -1,5 +1,5 @@
 """Build libhapi.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with
-the repo snapshot to the GPU box).  Usage: python -m paper_2210_08650_b200.build [--force]"""
+the repo snapshot to the GPU box).  Usage: python paper_2210_08650_b200/build.py [--force]"""
 from __future__ import annotations
 
 import glob

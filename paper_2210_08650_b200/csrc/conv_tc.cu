@@ -60,7 +60,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
+  uint32_t spins = 0;
   while (!done) {
+    // watchdog: a lost arrival must fail loudly instead of hanging the GPU
+    if (++spins == (1u << 30)) __trap();
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"

@@ -92,6 +92,7 @@ struct Op {
   const float* shift = nullptr;
   uint32_t kind = 0;             // plan_info kernel class
   double flops = 0, bytes = 0;   // per image
+  std::string desc;              // human-readable (hapi_plan_describe)
 };
 
 struct Buf {
@@ -119,6 +120,7 @@ struct hapi_model {
   cudaStream_t stream = nullptr;
   std::vector<ConvW> convs;
   std::map<std::string, int> conv_index;
+  std::map<std::string, std::pair<float*, float*>> bn_cache;  // unfused BN: device scale/shift
   std::vector<const float*> host_params;  // valid during create only
   std::vector<void*> allocs;
   int64_t weight_bytes = 0;
@@ -339,6 +341,11 @@ struct Builder {
     const double px = (double)out.H * out.W;
     o.flops = w.real_flops_per_px * px;
     o.bytes = ((double)in.H * in.W * (cs.linear ? in.C : cs.cin) + px * w.cout * (res ? 2 : 1)) * m->es;
+    char d[256];
+    std::snprintf(d, sizeof(d), "%s %dx%d/s%d C%d->%d %dx%d->%dx%d bn%d mode%d%s%s%s", cs.wname.c_str(), w.kh, w.kw,
+                  w.stride, w.cs, w.cout, in.H, in.W, out.H, out.W, w.bn, w.mode, relu ? " relu" : "", res ? " +res" : "",
+                  cs.pro_bn.empty() ? "" : " prologue");
+    o.desc = d;
     emit(o);
     if (op_out) *op_out = &p.ops.back();
     return HAPI_OK;
@@ -349,6 +356,10 @@ struct Builder {
     o.in = in; o.out = out; o.pk = k; o.ps = s; o.pp = pad; o.pmode = mode;
     o.kind = 2;
     o.bytes = ((double)in.H * in.W * in.C + (double)out.H * out.W * out.C) * m->es;
+    char d[128];
+    std::snprintf(d, sizeof(d), "%s %dx%d/s%d p%d C%d %dx%d->%dx%d", mode ? "avgpool" : "maxpool", k, k, s, pad, in.C,
+                  in.H, in.W, out.H, out.W);
+    o.desc = d;
     emit(o);
   }
 };
@@ -364,7 +375,7 @@ bool is_fresh_output(const Plan& p, int buf) {
   return refs == 1 && !p.ops.empty() && p.ops.back().out.buf == buf;
 }
 
-hapi_status build_plan(hapi_model* m, int split, Plan* out) {
+hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   Builder b{m};
   b.p.split = split;
   const ArchDesc& A = *m->arch;
@@ -417,11 +428,18 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out) {
           i += 3;
         } else {
           const bool relu = i + 1 < split && mods[i + 1].kind == MK_RELU;
-          std::vector<double> sc, sh;
-          if (!bn_affine(m, md.name, md.cin, sc, sh)) return set_error(HAPI_ERR_INVALID_MODEL, "bn %s", md.name.c_str());
-          std::vector<float> fsc(sc.begin(), sc.end()), fsh(sh.begin(), sh.end());
           float *dsc, *dsh;
-          if ((st = upload(m, fsc, &dsc)) != HAPI_OK || (st = upload(m, fsh, &dsh)) != HAPI_OK) return st;
+          auto it = m->bn_cache.find(md.name);
+          if (it != m->bn_cache.end()) {
+            dsc = it->second.first;
+            dsh = it->second.second;
+          } else {
+            std::vector<double> sc, sh;
+            if (!bn_affine(m, md.name, md.cin, sc, sh)) return set_error(HAPI_ERR_INVALID_MODEL, "bn %s", md.name.c_str());
+            std::vector<float> fsc(sc.begin(), sc.end()), fsh(sh.begin(), sh.end());
+            if ((st = upload(m, fsc, &dsc)) != HAPI_OK || (st = upload(m, fsh, &dsh)) != HAPI_OK) return st;
+            m->bn_cache[md.name] = {dsc, dsh};
+          }
           View o = b.compact(cur.C, cur.H, cur.W);
           Op op;
           op.t = OP_BNACT;
@@ -552,7 +570,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out) {
         View blk = b.compact(Ct, cur.H, cur.W);
         View head = blk;
         head.C = C0;
-        if (cur.buf >= 0 && is_fresh_output(b.p, cur.buf) && cur.ld == cur.C && cur.coff == 0) {
+        if (retarget && cur.buf >= 0 && is_fresh_output(b.p, cur.buf) && cur.ld == cur.C && cur.coff == 0) {
           // retarget the producing op (pool0 / transition pool) into the block buffer
           b.p.ops.back().out = head;
           b.p.bufs[cur.buf].per_img = 0;
@@ -794,12 +812,16 @@ hapi_status hapi_model_create(const hapi_model_desc* desc, const float* const* p
   }
   m->host_params.assign(params, params + n_params);
   for (uint32_t s = desc->min_split; s <= desc->max_split; ++s) {
-    Plan p;
-    hapi_status st = build_plan(m.get(), (int)s, &p);
+    // two candidate plans: pool written straight into the DenseNet block buffer (fewer
+    // launches) or through a compact buffer + copy (lower peak); keep the smaller arena
+    Plan p, p2;
+    hapi_status st = build_plan(m.get(), (int)s, &p, true);
+    if (st == HAPI_OK) st = build_plan(m.get(), (int)s, &p2, false);
     if (st != HAPI_OK) {
       hapi_model_destroy(m.release());
       return st;
     }
+    if (p2.arena_bytes < p.arena_bytes) p = std::move(p2);
     m->arena_bytes = std::max(m->arena_bytes, p.arena_bytes);
     m->plans.push_back(std::move(p));
   }
@@ -909,6 +931,19 @@ hapi_status hapi_model_device_bytes(const hapi_model* m, uint64_t* wb, uint64_t*
   if (!m) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null model");
   if (wb) *wb = (uint64_t)m->weight_bytes;
   if (ab) *ab = (uint64_t)m->arena_bytes;
+  return HAPI_OK;
+}
+
+hapi_status hapi_plan_describe(const hapi_model* m, uint32_t split_idx, uint32_t op, char* buf, uint32_t cap) {
+  clear_error();
+  if (!m || !buf || cap == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (split_idx < m->d.min_split || split_idx > m->d.max_split) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx");
+  const Plan& p = m->plans[split_idx - m->d.min_split];
+  if (op >= p.ops.size()) return set_error(HAPI_ERR_INVALID_ARGUMENT, "op index");
+  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out"};
+  const Op& o = p.ops[op];
+  std::snprintf(buf, cap, "%s%s%s", o.desc.empty() ? names[o.t] : o.desc.c_str(), o.out.buf < 0 ? " ->out" : "",
+                o.nchw_out ? "(nchw)" : "");
   return HAPI_OK;
 }
 

@@ -1,0 +1,176 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element on
+the same seeded inputs.  Tolerances are BASELINE.json's north_star: relative L2 <= 1e-5
+on the fp32 path and <= 2e-2 on the bf16 tensor-core path (reading A21: over the whole
+split output of the call, fp64).  Shapes/bytes, split choices and batch sizes are exact.
+"""
+import numpy as np
+import pytest
+
+import hapi_inputs
+from oracle import archs, planner
+from tests.gpu_helpers import gpu_forward, oracle_all, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-5, "bf16": 2e-2}
+SMALL = {"alexnet": 224, "resnet18": 64, "resnet50": 96, "vgg11": 64, "densenet121": 64}
+
+
+def _H():
+    import paper_2210_08650_b200 as H
+    return H
+
+
+@pytest.mark.parametrize("act", ["f32", "bf16"])
+@pytest.mark.parametrize("arch", list(archs.ARCHS))
+def test_every_split_small(arch, act):
+    """Every canonical split s = 1..L (fusion legality at every boundary, H3), ragged tiles."""
+    H = _H()
+    sz, n = SMALL[arch], 3
+    P = hapi_inputs.params(arch, 21)
+    x = hapi_inputs.images(n, 22, sz, sz)
+    L = len(archs.layers(arch))
+    ref = oracle_all(arch, 21, 22, n, sz, sz)
+    model = H.Model(arch, act, list(P.values()), n, 1, L, in_h=sz, in_w=sz)
+    for s in range(1, L + 1):
+        got, _ = gpu_forward(arch, act, s, x, P, model=model)
+        want = ref[s - 1].reshape(n, -1)
+        assert got.shape == want.shape
+        assert model.out_bytes[s - 1] == want.shape[1] * (4 if act == "f32" else 2)
+        e = rel_l2(got, want)
+        assert e <= TOL[act], (arch, act, s, e)
+    model.close()
+
+
+def test_config1_alexnet_fp32_full_batch():
+    """configs[0]: AlexNet features prefix s=13, batch 8, fp32, full-batch parity."""
+    P = hapi_inputs.params("alexnet", 1001)
+    x = hapi_inputs.images(8, 1)
+    got, m = gpu_forward("alexnet", "f32", 13, x, P)
+    ref = oracle_all("alexnet", 1001, 1, 8, upto=13)[12].reshape(8, -1)
+    assert got.shape == (8, 9216)
+    assert rel_l2(got, ref) <= 1e-5
+    for i in range(8):
+        assert rel_l2(got[i], ref[i]) <= 1e-5
+
+
+SAMPLE = {"resnet18": (200, [0, 1, 198, 199]), "resnet50": (512, [0, 1, 510, 511])}
+
+
+@pytest.mark.parametrize("arch,split", [("resnet18", 10), ("resnet50", 21), ("resnet50", 20)])
+def test_configs_2_3_bench_size_sampled(arch, split):
+    """configs[1]/[2] at the bench's launch configuration (batch 200 / 512): sampled
+    outputs checked against the oracle one by one, and batch invariance (bitwise) ties the
+    sampled images to their rows of the full-batch launch."""
+    H = _H()
+    batch, sel = SAMPLE[arch]
+    seed = 2 if arch == "resnet18" else 3
+    P = hapi_inputs.params(arch, 1000 + seed)
+    x = hapi_inputs.images(batch, seed)
+    model = H.Model(arch, "bf16", list(P.values()), batch, split, split)
+    got, _ = gpu_forward(arch, "bf16", split, x, P, model=model)
+    ref = oracle_all(arch, 1000 + seed, seed, batch, upto=split, sel=sel)[split - 1].reshape(len(sel), -1)
+    assert rel_l2(got[sel], ref) <= 2e-2
+    for j, i in enumerate(sel):
+        assert rel_l2(got[i], ref[j]) <= 2e-2
+    small, _ = gpu_forward(arch, "bf16", split, np.ascontiguousarray(x[sel]), P, model=model)
+    np.testing.assert_array_equal(small, got[sel])
+    assert np.isfinite(got).all()
+    model.close()
+
+
+def _free_hbm():
+    import torch
+    return torch.cuda.mem_get_info()[0]
+
+
+@pytest.mark.parametrize("arch,splits", [("vgg11", [11] + list(range(16, 26))),
+                                         ("densenet121", [4, 9] + list(range(13, 21)))])
+def test_config4_split_sweep_budgeted(arch, splits):
+    """configs[3]: bf16 split sweep over the candidate layers with the HBM-budgeted COS
+    batch (budgets: free HBM, 16 GiB = the paper's T4, 2 GiB).  Split/batch choices come
+    from hapi_choose_split and must equal the oracle planner; activations within 2e-2;
+    library-owned device bytes <= est(b, s) (reading R8)."""
+    H = _H()
+    P = hapi_inputs.params(arch, 1004)
+    n = 2
+    x = hapi_inputs.images(n, 4)
+    ref = oracle_all(arch, 1004, 4, n, upto=max(splits))
+    for budget in (_free_hbm() // 2, 16 << 30, 2 << 30):
+        for s in splits:
+            # freeze = s and a 1 B/s link: no candidate passes, Alg. 1 returns the freeze index s
+            st, r, _ = H.hapi_choose_split(arch, s, 2000, 1, budget, b_min=25, b_max=2000, act="bf16")
+            q = planner.choose_split(planner.SplitQuery(arch, s, 2000, 1, budget, b_min=25, b_max=2000, act="bf16"))
+            assert (st, r["split_idx"], r["cos_batch"], r["est_bytes"]) == (q.status, q.split_idx, q.cos_batch,
+                                                                             q.est_bytes)
+            assert r["split_idx"] == s
+            b = r["cos_batch"]
+            model = H.Model(arch, "bf16", list(P.values()), b, s, s)
+            wb, ab = model.device_bytes()
+            est = planner.estimate(arch, s, b, "bf16")
+            assert wb + ab <= est, (arch, s, b, wb, ab, est)
+            if budget == (2 << 30):
+                got, _ = gpu_forward(arch, "bf16", s, x, P, model=model)
+                e = rel_l2(got, ref[s - 1].reshape(n, -1))
+                assert e <= 2e-2, (arch, s, e)
+            model.close()
+
+
+@pytest.mark.parametrize("arch,split,act", [("resnet50", 21, "bf16"), ("alexnet", 13, "f32"), ("resnet18", 10, "bf16"),
+                                            ("densenet121", 9, "bf16"), ("resnet50", 4, "bf16")])
+def test_memory_bound(arch, split, act):
+    """Device bytes owned by the model <= est(b, s) = W(s) + b*P(s) (section 4.3 'we
+    always over-estimate')."""
+    H = _H()
+    P = hapi_inputs.params(arch, 7)
+    for b in (1, 25, 200):
+        model = H.Model(arch, act, list(P.values()), b, split, split)
+        wb, ab = model.device_bytes()
+        assert wb + ab <= planner.estimate(arch, split, b, act), (b, wb, ab)
+        model.close()
+
+
+@pytest.mark.parametrize("act", ["bf16", "f32"])
+def test_chunking_batch_shard_invariance_determinism(act):
+    """a8 + H6: chunked (batch > max_batch), sharded (contiguous ranges) and
+    repeated runs give bit-identical outputs."""
+    H = _H()
+    arch, s, n = "resnet50", 21, 7
+    P = hapi_inputs.params(arch, 8)
+    x = hapi_inputs.images(n, 9, 96, 96)
+    big = H.Model(arch, act, list(P.values()), n, s, s, in_h=96, in_w=96)
+    small = H.Model(arch, act, list(P.values()), 3, s, s, in_h=96, in_w=96)
+    full, _ = gpu_forward(arch, act, s, x, P, model=big)
+    again, _ = gpu_forward(arch, act, s, x, P, model=big)
+    chunked, _ = gpu_forward(arch, act, s, x, P, model=small)
+    np.testing.assert_array_equal(full, again)
+    np.testing.assert_array_equal(full, chunked)
+    shards = [gpu_forward(arch, act, s, np.ascontiguousarray(x[a:b]), P, model=big)[0]
+              for a, b in [(0, 2), (2, 5), (5, 7)]]
+    np.testing.assert_array_equal(np.concatenate(shards), full)
+
+
+def test_host_path_equals_device_path():
+    H = _H()
+    arch, s, n = "resnet18", 10, 9
+    P = hapi_inputs.params(arch, 10)
+    x = hapi_inputs.images(n, 11, 64, 64)
+    m = H.Model(arch, "bf16", list(P.values()), 4, s, s, in_h=64, in_w=64)
+    dev, _ = gpu_forward(arch, "bf16", s, x, P, model=m)
+    host, _ = gpu_forward(arch, "bf16", s, x, P, model=m, host=True)
+    np.testing.assert_array_equal(dev, host)
+
+
+def test_gpu_argument_errors():
+    import torch
+    H = _H()
+    P = hapi_inputs.params("alexnet", 0)
+    m = H.Model("alexnet", "f32", list(P.values()), 2, 5, 13)
+    x = torch.zeros(2, 3, 224, 224, device="cuda")
+    out = torch.zeros(2 * 200000, device="cuda")
+    for bad in (4, 14):
+        with pytest.raises(H.HapiError) as e:
+            m.forward(bad, x, out)
+        assert e.value.status == 1
+    with pytest.raises(H.HapiError):
+        m.forward(13, x[:0], out)
