@@ -297,7 +297,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, dt, threads = cpu_oracle_rate(arch, split, seed, 1)
-        n2 = max(1, min(8, int(15.0 / max(dt, 1e-3))))
+        n2 = max(1, min(64, int(15.0 / max(dt, 1e-3))))
         if n2 > 1:
             rate, dt, threads = cpu_oracle_rate(arch, split, seed, n2)
         cpu = {"value": rate, "unit": "img/s", "cores": threads, "kind": "oracle",

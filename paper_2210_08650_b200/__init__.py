@@ -111,9 +111,10 @@ class Model:
         self.out_bytes = hapi_layer_sizes(arch, in_h, in_w, act)[1]
 
     def close(self):
-        if getattr(self, "_h", None):
-            _lib.hapi_model_destroy(self._h)
-            self._h = None
+        h = getattr(self, "_h", None)
+        if h and _lib is not None and getattr(_lib, "hapi_model_destroy", None) is not None:
+            _lib.hapi_model_destroy(h)
+        self._h = None
 
     __del__ = close
 

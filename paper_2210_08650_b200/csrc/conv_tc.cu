@@ -7,15 +7,27 @@
 // (PAPER.md:732); the paper ran it as cuDNN calls on T4 -- this is a B200-first design.
 //
 //   GEMM view: D[M=N*OH*OW][Cout] = A[M][K] * B[Cout][K]^T, K = KH*KW*C ordered (r, s, c).
-//   A = activations gathered from NHWC (implicit im2col), B = packed bf16 weights.
+//   A = activations (implicit im2col of NHWC), B = packed bf16 weights [Cout][Kp].
 //
-// Persistent, warp-specialized CTA (one per SM, 288 threads):
-//   warps 0-3  epilogue: TMEM -> registers (tcgen05.ld) -> bias/residual/ReLU -> bf16 store
-//   warps 4-7  producer: A tile gather into 128B-swizzled smem (cp.async or a register
-//              path for the bn-relu prologue); thread 0 also issues the B tile TMA
+// Persistent, warp-specialized CTA (one per SM, 320 threads):
+//   warps 0-3  epilogue: thread = tile row (its TMEM lane).  Per 64-column block:
+//              tcgen05.ld -> + bias (smem) + residual (swizzled smem block) -> ReLU ->
+//              bf16 into a 128B-swizzled staging block (conflict-free) -> one TMA store
+//              (2D [M][C] box, or the 4D spatial box of mode 4); NCHW send-buffer writes
+//              of the split layer go straight from registers (coalesced per channel)
+//   warps 4-7  producer.  A operand per K chunk (one filter tap x 64 channels):
+//                mode 3  TMA 2D box {64 ch, 128 rows} of the [M][C] matrix (1x1, stride 1)
+//                mode 4  TMA 4D box {64 ch, wb, hb, nb} of the NHWC tensor shifted by the tap
+//                        (traversal stride = conv stride; OOB zero fill = conv padding)
+//                mode 0  cp.async 16-byte gather (C % 8 == 0: stems)
+//                mode 2  register gather with the DenseNet bn-relu prologue
+//              B operand: TMA 2D box {64, BN} of the weights.  Both 128-byte swizzled.
 //   warp 8     TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
-// Pipelines: smem ring of STAGES (full/empty mbarriers), two TMEM accumulators
-// (tfull/tempty) so the epilogue of tile i overlaps the MMAs of tile i+1.
+//   warp 9     residual loader: TMA of the residual blocks into a 2-deep smem ring
+// Pipelines: smem ring of STAGES (full/empty mbarriers, depth chosen per launch from the
+// smem left after the epilogue buffers), two TMEM accumulators (tfull/tempty) so the
+// epilogue of tile i overlaps the MMAs of tile i+1, residual ring (rfull/rempty), and
+// double-buffered TMA-store staging (bulk async-groups).
 #include <cuda_bf16.h>
 
 #include "kernels.h"
@@ -29,18 +41,28 @@ constexpr int NUM_EPI_WARPS = 4;
 constexpr int PROD_WARP0 = 4;
 constexpr int NUM_PROD_THREADS = 128;
 constexpr int MMA_WARP = 8;
-constexpr int NUM_THREADS = 9 * 32;
+constexpr int RES_WARP = 9;
+constexpr int NUM_THREADS = 10 * 32;
 constexpr int A_STAGE_BYTES = BM * BK * 2;
+constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in per CTA
+constexpr int MAX_STAGES = 8;
 
+// Static part of the shared-memory carve-up; the pipeline depth is chosen per launch.
 template <int BN>
 struct Cfg {
+  static constexpr int SB = BN < 64 ? BN : 64;               // epilogue block width (columns)
+  static constexpr int SB_BYTES = SB * 2 * BM;               // one [128 x SB] bf16 block (swizzled)
+  static constexpr int SWZ = SB * 2;                         // 64- or 128-byte swizzle of that block
   static constexpr int B_STAGE_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 512 /*barriers*/;
+  static int stages(bool res) {
+    int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
+    return s > MAX_STAGES ? MAX_STAGES : s;
+  }
+  static int smem_bytes(int stages, bool res) { return stages * STAGE_BYTES + FIXED + (res ? 2 * SB_BYTES : 0); }
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -76,9 +98,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_size) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_size) : "memory");
 }
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src, uint32_t src_size) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_size) : "memory");
-}
 // Arrive on `bar` once all prior cp.async of this thread have landed (pending count is
 // incremented first, so this does not consume one of the barrier's expected arrivals).
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
@@ -93,6 +112,30 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -100,7 +143,6 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);        // start address
-  d |= (uint64_t)(0) << 16;                      // leading byte offset (unused, swizzled K-major)
   d |= (uint64_t)(1024 >> 4) << 32;              // stride byte offset between 8-row groups
   d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
@@ -141,38 +183,96 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
   return __bfloat1622float2(h);
 }
 
+// Tile geometry shared by producer, epilogue and loaders.
+struct Geo {
+  int mode;
+  int wb, hb, nb;              // mode 4 spatial tile
+  int tiles_w, tiles_h;        // mode 4
+  int m_tiles, n_tiles, k_chunks, cblocks;
+  int a_bytes;                 // TMA modes: bytes of one A box
+  int stages;                  // smem pipeline depth
+  int has_res;                 // residual tiles streamed by the loader warp
+  int tma_out;                 // 1: epilogue writes via TMA store (NHWC views); 0: NCHW direct
+  int res_box_bytes;           // bytes of one residual box
+};
+
+// Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
+__device__ __forceinline__ long long row_to_m(const ConvArgs& a, const Geo& g, int tm, int i) {
+  if (g.mode != 4) {
+    const long long m = (long long)tm * BM + i;
+    return m < a.M ? m : -1;
+  }
+  const int per_img = g.hb * g.wb;
+  if (i >= g.nb * per_img) return -1;
+  const int tw = tm % g.tiles_w;
+  const int th = (tm / g.tiles_w) % g.tiles_h;
+  const int tb = tm / (g.tiles_w * g.tiles_h);
+  const int ni = i / per_img, rem = i - ni * per_img;
+  const int hi = rem / g.wb, wi = rem - hi * g.wb;
+  const int n = tb * g.nb + ni, oh = th * g.hb + hi, ow = tw * g.wb + wi;
+  if (n >= a.N || oh >= a.OH || ow >= a.OW) return -1;
+  return ((long long)n * a.OH + oh) * a.OW + ow;
+}
+
+// Spatial origin of m-tile tm in mode 4 (output coordinates).
+__device__ __forceinline__ void tile_origin(const Geo& g, int tm, int* w0, int* h0, int* b0) {
+  const int tw = tm % g.tiles_w, th = (tm / g.tiles_w) % g.tiles_h, tb = tm / (g.tiles_w * g.tiles_h);
+  *w0 = tw * g.wb;
+  *h0 = th * g.hb;
+  *b0 = tb * g.nb;
+}
+
+// Byte offset of 16-byte chunk `c` of row `r` inside a [rows x SWZ-byte] swizzled block.
+template <int SWZ>
+__device__ __forceinline__ uint32_t swz_off(int r, int c) {
+  if (SWZ == 128) return r * 128 + ((c ^ (r & 7)) << 4);
+  return r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+}
+
 // ------------------------------------------------------------------ the kernel
 template <int BN, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-    conv_tc_kernel(const ConvArgs a, const __grid_constant__ CUtensorMap tmap_b, int m_tiles, int n_tiles,
-                   int k_chunks) {
+    conv_tc_kernel(const ConvArgs a, const Geo g, const __grid_constant__ CUtensorMap tmap_a,
+                   const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_y,
+                   const __grid_constant__ CUtensorMap tmap_r) {
   using C = Cfg<BN>;
+  constexpr int SB = C::SB;
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4);
+  const int S = g.stages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * A_STAGE_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
+  uint8_t* sB = sA + S * A_STAGE_BYTES;
+  uint8_t* sY = sB + S * C::B_STAGE_BYTES;                 // 2 output staging blocks
+  uint8_t* sR = sY + 2 * C::SB_BYTES;                      // 2 residual blocks (if has_res)
+  float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? 2 * C::SB_BYTES : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(sBias + BN);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], NUM_PROD_THREADS + 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], TMA_A ? 1 : NUM_PROD_THREADS + 1);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], NUM_EPI_WARPS * 32);
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], NUM_EPI_WARPS * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == PROD_WARP0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+    if (TMA_A) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
   }
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -185,61 +285,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_tiles = m_tiles * n_tiles;
+  const int num_tiles = g.m_tiles * g.n_tiles;
   const int OHW = a.OH * a.OW;
 
   if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ producer
     const int pt = threadIdx.x - PROD_WARP0 * 32;
-    const char* xb = static_cast<const char*>(a.x);
-    const int taps = a.KH * a.KW;
-    uint32_t stage = 0, phase = 0;
-    constexpr int ROWS = (MODE == 1) ? 16 : 8;       // rows handled per thread
-    constexpr int RSTEP = (MODE == 1) ? 8 : 16;      // row stride between them
-    const int q = (MODE == 1) ? (pt & 15) : (pt & 7);  // piece index within a 128 B row
-    const int rsub = (MODE == 1) ? (pt >> 4) : (pt >> 3);
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int tm = tile / n_tiles, tn = tile - (tile / n_tiles) * n_tiles;
-      int ih0[ROWS], iw0[ROWS];
-      long long ioff[ROWS];
-#pragma unroll
-      for (int i = 0; i < ROWS; ++i) {
-        const long long m = (long long)tm * BM + rsub + RSTEP * i;
-        if (m < a.M) {
-          const int n = (int)(m / OHW);
-          const int rem = (int)(m - (long long)n * OHW);
-          const int oh = rem / a.OW, ow = rem - (rem / a.OW) * a.OW;
-          ih0[i] = oh * a.stride - a.pad;
-          iw0[i] = ow * a.stride - a.pad;
-          ioff[i] = (long long)n * a.H * a.W;
-        } else {
-          ih0[i] = -(1 << 28);
-          iw0[i] = 0;
-          ioff[i] = 0;
+    if (TMA_A) {
+      if (pt == 0) {
+        uint32_t stage = 0, phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+          const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+          int w0 = 0, h0 = 0, b0 = 0;
+          if (MODE == 4) {
+            tile_origin(g, tm, &w0, &h0, &b0);
+            w0 = w0 * a.stride - a.pad;
+            h0 = h0 * a.stride - a.pad;
+          }
+          for (int kc = 0; kc < g.k_chunks; ++kc) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], g.a_bytes + C::B_STAGE_BYTES);
+            const uint32_t dA = smem_u32(sA + stage * A_STAGE_BYTES);
+            if (MODE == 3) {
+              tma_load_2d(dA, &tmap_a, kc * BK, tm * BM, &full[stage]);
+            } else {
+              const int tap = kc / g.cblocks, cb = kc - tap * g.cblocks;
+              const int r = tap / a.KW, s = tap - r * a.KW;
+              tma_load_4d(dA, &tmap_a, cb * BK, w0 + s, h0 + r, b0, &full[stage]);
+            }
+            tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, kc * BK, tn * BN, &full[stage]);
+            if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+          }
         }
       }
-      for (int kc = 0; kc < k_chunks; ++kc) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (pt == 0) {
-          mbar_arrive_expect_tx(&full[stage], C::B_STAGE_BYTES);
-          tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, kc * BK, tn * BN, &full[stage]);
-        }
-        const uint32_t a_stage = smem_u32(sA + stage * A_STAGE_BYTES);
-        if (MODE == 1) {
-          // stem: C == 4, one 8-byte piece = one filter tap
-          const int tap = kc * 16 + q;
-          const int r = tap / a.KW, s = tap - (tap / a.KW) * a.KW;
-          const bool tap_ok = tap < taps;
-          const uint32_t dst0 = a_stage + rsub * 128 + ((((q >> 1) ^ (rsub & 7))) << 4) + (q & 1) * 8;
+    } else {
+      const char* xb = static_cast<const char*>(a.x);
+      const int taps = a.KH * a.KW;
+      uint32_t stage = 0, phase = 0;
+      const int q = pt & 7;          // 16-byte piece index within a 128-byte row
+      const int rsub = pt >> 3;      // rows rsub + 16 i
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+        int ih0[8], iw0[8];
+        long long ioff[8];
 #pragma unroll
-          for (int i = 0; i < ROWS; ++i) {
-            const int ih = ih0[i] + r, iw = iw0[i] + s;
-            const bool ok = tap_ok && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
-            const char* src = ok ? xb + ((ioff[i] + (long long)ih * a.W + iw) * a.x_ld) * 2 : xb;
-            cp_async8(dst0 + i * 1024, src, ok ? 8u : 0u);
+        for (int i = 0; i < 8; ++i) {
+          const long long m = (long long)tm * BM + rsub + 16 * i;
+          if (m < a.M) {
+            const int n = (int)(m / OHW);
+            const int rem = (int)(m - (long long)n * OHW);
+            const int oh = rem / a.OW, ow = rem - (rem / a.OW) * a.OW;
+            ih0[i] = oh * a.stride - a.pad;
+            iw0[i] = ow * a.stride - a.pad;
+            ioff[i] = (long long)n * a.H * a.W;
+          } else {
+            ih0[i] = -(1 << 28);
+            iw0[i] = 0;
+            ioff[i] = 0;
           }
-          cp_async_mbar_arrive(&full[stage]);
-        } else {
+        }
+        for (int kc = 0; kc < g.k_chunks; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (pt == 0) {
+            mbar_arrive_expect_tx(&full[stage], C::B_STAGE_BYTES);
+            tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, kc * BK, tn * BN, &full[stage]);
+          }
+          const uint32_t a_stage = smem_u32(sA + stage * A_STAGE_BYTES);
           const int k0 = kc * BK + q * 8;
           const int tap = k0 / a.C;
           const int c = k0 - tap * a.C;
@@ -248,7 +359,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t dst0 = a_stage + rsub * 128 + ((q ^ (rsub & 7)) << 4);
           if (MODE == 0) {
 #pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
+            for (int i = 0; i < 8; ++i) {
               const int ih = ih0[i] + r, iw = iw0[i] + s;
               const bool ok = tap_ok && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
               const char* src = ok ? xb + ((ioff[i] + (long long)ih * a.W + iw) * a.x_ld + c) * 2 : xb;
@@ -257,10 +368,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             cp_async_mbar_arrive(&full[stage]);
           } else {
             // bn-relu prologue: A := relu(x * scale[c] + shift[c]); padding stays zero
-            uint4 raw[ROWS];
-            bool okv[ROWS];
+            uint4 raw[8];
+            bool okv[8];
 #pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
+            for (int i = 0; i < 8; ++i) {
               const int ih = ih0[i] + r, iw = iw0[i] + s;
               okv[i] = tap_ok && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W;
               raw[i] = make_uint4(0, 0, 0, 0);
@@ -282,28 +393,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < 8; ++j) { sc[j] = 0.f; sh[j] = 0.f; }
             }
 #pragma unroll
-            for (int i = 0; i < ROWS; ++i) {
-              uint32_t w4[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
-              uint4 o = make_uint4(0, 0, 0, 0);
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t w4[4] = {raw[i].x, raw[i].y, raw[i].z, raw[i].w};
+              uint32_t ov[4] = {0u, 0u, 0u, 0u};
               if (okv[i]) {
-                uint32_t ov[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                   const float2 f = unpack_bf16x2(w4[j]);
                   ov[j] = pack_bf16x2(fmaxf(fmaf(f.x, sc[2 * j], sh[2 * j]), 0.f),
                                       fmaxf(fmaf(f.y, sc[2 * j + 1], sh[2 * j + 1]), 0.f));
                 }
-                o = make_uint4(ov[0], ov[1], ov[2], ov[3]);
               }
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst0 + i * 2048), "r"(o.x), "r"(o.y),
-                           "r"(o.z), "r"(o.w)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst0 + i * 2048), "r"(ov[0]), "r"(ov[1]),
+                           "r"(ov[2]), "r"(ov[3])
                            : "memory");
             }
             fence_proxy_async_smem();
           }
+          mbar_arrive(&full[stage]);
+          if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
         }
-        mbar_arrive(&full[stage]);
-        if (++stage == (uint32_t)C::STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == MMA_WARP) {
@@ -320,7 +429,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kc = 0; kc < k_chunks; ++kc) {
+        for (int kc = 0; kc < g.k_chunks; ++kc) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = make_sdesc(smem_u32(sA + stage * A_STAGE_BYTES));
@@ -331,94 +440,158 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
           }
           mma_commit(&empty[stage]);
-          if (kc == k_chunks - 1) mma_commit(&tfull[acc]);
-          if (++stage == (uint32_t)C::STAGES) { stage = 0; phase ^= 1; }
+          if (kc == g.k_chunks - 1) mma_commit(&tfull[acc]);
+          if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
         }
       }
     }
     __syncwarp();
+  } else if (warp == RES_WARP) {
+    // ================================================================ residual loader
+    // Streams the [128 x SB] residual blocks of every output tile, in the order the
+    // epilogue consumes them, into a 2-deep smem ring (TMA, same swizzle as the staging).
+    if (g.has_res && lane == 0) {
+      uint32_t rs = 0, rph = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+        int w0 = 0, h0 = 0, b0 = 0;
+        if (MODE == 4) tile_origin(g, tm, &w0, &h0, &b0);
+        for (int jb = 0; jb < BN; jb += SB) {
+          const int n0 = tn * BN + jb;
+          if (n0 >= a.Cout) break;
+          mbar_wait(&rempty[rs], rph ^ 1);
+          mbar_arrive_expect_tx(&rfull[rs], g.res_box_bytes);
+          const uint32_t dst = smem_u32(sR + rs * C::SB_BYTES);
+          if (MODE == 4)
+            tma_load_4d(dst, &tmap_r, n0, w0, h0, b0, &rfull[rs]);
+          else
+            tma_load_2d(dst, &tmap_r, n0, tm * BM, &rfull[rs]);
+          if (++rs == 2) { rs = 0; rph ^= 1; }
+        }
+      }
+    }
   } else {
     // ================================================================ epilogue
+    // Thread = tile row (its TMEM lane).  Per SB-column block: TMEM -> registers, + bias
+    // (smem) + residual (TMA-prefetched swizzled smem block), ReLU, bf16 -> swizzled
+    // staging block (conflict-free 16-byte stores) -> one TMA store per block.
     const int row = warp * 32 + lane;
+    const int et = threadIdx.x;  // 0..127
     __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.y);
     const __nv_bfloat16* rb = static_cast<const __nv_bfloat16*>(a.res);
-    const bool vec_y = !a.nchw && ((reinterpret_cast<uintptr_t>(a.y) & 15) == 0) && (a.y_ld % 8 == 0);
-    const bool vec_r = rb && ((reinterpret_cast<uintptr_t>(a.res) & 15) == 0) && (a.res_ld % 8 == 0);
+    uint32_t rs = 0, rph = 0;
+    int blk = 0;
     int iter = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
-      const int tm = tile / n_tiles, tn = tile - (tile / n_tiles) * n_tiles;
+      const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
+      // bias of this tile's columns -> smem (the previous tile's readers are past the
+      // last epi_bar of that tile)
+      for (int j = et; j < BN; j += 128) {
+        const int n = tn * BN + j;
+        sBias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const long long m = (long long)tm * BM + row;
-      const bool mok = m < a.M;
-      int img = 0, pix = 0;
-      if (a.nchw && mok) {
-        img = (int)(m / OHW);
-        pix = (int)(m - (long long)img * OHW);
-      }
+      const uint32_t t_row = tmem_base + ((uint32_t)(warp * 32) << 16) + acc * BN;
+      if (!g.tma_out) {
+        // final layer straight into the NCHW send buffer (consecutive rows = consecutive
+        // pixels, so thread-per-row stores are coalesced per channel)
+        epi_bar();
+        const long long m = row_to_m(a, g, tm, row);
+        int img = 0, pix = 0;
+        if (m >= 0) {
+          img = (int)(m / OHW);
+          pix = (int)(m - (long long)img * OHW);
+        }
 #pragma unroll 1
-      for (int j0 = 0; j0 < BN; j0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(warp * 32) << 16) + acc * BN + j0, v);
-        tmem_wait_ld();
-        const int n0 = tn * BN + j0;
-        if (!mok || n0 >= a.Cout) continue;
-        const int nv = min(32, a.Cout - n0);
-        float f[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
-        if (a.bias) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < nv) f[j] += __ldg(a.bias + n0 + j);
-        }
-        if (rb) {
-          const __nv_bfloat16* rp = rb + m * a.res_ld + n0;
-          if (vec_r && nv == 32) {
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const uint4 u = __ldg(reinterpret_cast<const uint4*>(rp) + q4);
-              const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float2 g = unpack_bf16x2(uu[j]);
-                f[q4 * 8 + 2 * j] += g.x;
-                f[q4 * 8 + 2 * j + 1] += g.y;
-              }
-            }
-          } else {
-            for (int j = 0; j < nv; ++j) f[j] += __bfloat162float(rp[j]);
-          }
-        }
-        if (a.relu) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) f[j] = fmaxf(f[j], 0.f);
-        }
-        if (a.nchw) {
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(t_row + j0, v);
+          tmem_wait_ld();
+          const int n0 = tn * BN + j0;
+          if (m < 0 || n0 >= a.Cout) continue;
           __nv_bfloat16* yp = yb + ((long long)img * a.Cout + n0) * OHW + pix;
-          for (int j = 0; j < nv; ++j) yp[(long long)j * OHW] = __float2bfloat16_rn(f[j]);
-        } else {
-          __nv_bfloat16* yp = yb + m * a.y_ld + n0;
-          if (vec_y && nv == 32) {
+          const __nv_bfloat16* rp = rb ? rb + m * a.res_ld + n0 : nullptr;
 #pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint4 o;
-              o.x = pack_bf16x2(f[q4 * 8 + 0], f[q4 * 8 + 1]);
-              o.y = pack_bf16x2(f[q4 * 8 + 2], f[q4 * 8 + 3]);
-              o.z = pack_bf16x2(f[q4 * 8 + 4], f[q4 * 8 + 5]);
-              o.w = pack_bf16x2(f[q4 * 8 + 6], f[q4 * 8 + 7]);
-              reinterpret_cast<uint4*>(yp)[q4] = o;
+          for (int j = 0; j < 32; ++j) {
+            if (n0 + j < a.Cout) {
+              float f = __uint_as_float(v[j]) + sBias[j0 + j];
+              if (rp) f += __bfloat162float(rp[j]);
+              if (a.relu) f = fmaxf(f, 0.f);
+              yp[(long long)j * OHW] = __float2bfloat16_rn(f);
             }
-          } else {
-            for (int j = 0; j < nv; ++j) yp[j] = __float2bfloat16_rn(f[j]);
           }
+        }
+        epi_bar();
+      } else {
+        int w0 = 0, h0 = 0, b0 = 0;
+        if (MODE == 4) tile_origin(g, tm, &w0, &h0, &b0);
+        for (int jb = 0; jb < BN; jb += SB) {
+          const int n0 = tn * BN + jb;
+          if (n0 >= a.Cout) break;  // uniform
+          const int buf = blk & 1;
+          const uint32_t stg = smem_u32(sY + buf * C::SB_BYTES);
+          // staging block `buf` was last stored two blocks ago: wait until TMA read it
+          if (et == 0) bulk_wait_read1();
+          epi_bar();
+          if (g.has_res) mbar_wait(&rfull[rs], rph);
+          const uint32_t rsm = smem_u32(sR + rs * C::SB_BYTES);
+#pragma unroll
+          for (int sub = 0; sub < SB / 32; ++sub) {
+            uint32_t v[32];
+            tmem_ld32(t_row + jb + sub * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {  // 8 columns = one 16-byte chunk
+              const int chunk = sub * 4 + c4;
+              float f[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c4 * 8 + j]) + sBias[jb + chunk * 8 + j];
+              if (g.has_res) {
+                uint32_t r0, r1, r2, r3;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                             : "r"(rsm + swz_off<C::SWZ>(row, chunk)));
+                const uint32_t rr[4] = {r0, r1, r2, r3};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 r2f = unpack_bf16x2(rr[j]);
+                  f[2 * j] += r2f.x;
+                  f[2 * j + 1] += r2f.y;
+                }
+              }
+              if (a.relu) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
+              }
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + swz_off<C::SWZ>(row, chunk)),
+                           "r"(pack_bf16x2(f[0], f[1])), "r"(pack_bf16x2(f[2], f[3])), "r"(pack_bf16x2(f[4], f[5])),
+                           "r"(pack_bf16x2(f[6], f[7]))
+                           : "memory");
+            }
+          }
+          if (g.has_res) {
+            mbar_arrive(&rempty[rs]);
+            if (++rs == 2) { rs = 0; rph ^= 1; }
+          }
+          fence_proxy_async_smem();
+          epi_bar();
+          if (et == 0) {
+            if (MODE == 4)
+              tma_store_4d(&tmap_y, stg, n0, w0, h0, b0);
+            else
+              tma_store_2d(&tmap_y, stg, n0, tm * BM);
+            bulk_commit();
+          }
+          ++blk;
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
+    if (et == 0) bulk_wait_all();
   }
 
   tc_fence_before();
@@ -431,31 +604,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 template <int BN, int MODE>
-cudaError_t launch_t(const ConvArgs& a, const CUtensorMap* tmap, int num_sms, cudaStream_t st) {
+cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, cudaStream_t st) {
   using C = Cfg<BN>;
   static bool attr_set = false;  // per-instantiation; benign race (idempotent)
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+                                         SMEM_LIMIT);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int m_tiles = (int)((a.M + BM - 1) / BM);
-  const int n_tiles = (a.Cout + BN - 1) / BN;
-  const int k_chunks = (a.K + BK - 1) / BK;
-  const int tiles = m_tiles * n_tiles;
+  g.stages = C::stages(g.has_res);
+  g.res_box_bytes = g.mode == 4 ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
+  const int smem = C::smem_bytes(g.stages, g.has_res);
+  const int tiles = g.m_tiles * g.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
-  conv_tc_kernel<BN, MODE><<<grid, NUM_THREADS, C::SMEM_BYTES, st>>>(a, *tmap, m_tiles, n_tiles, k_chunks);
+  const CUtensorMap* b = mp.b;
+  conv_tc_kernel<BN, MODE><<<grid, NUM_THREADS, smem, st>>>(a, g, mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b,
+                                                            mp.r ? *mp.r : *b);
   return cudaGetLastError();
 }
 
 template <int BN>
-cudaError_t launch_mode(const ConvArgs& a, const CUtensorMap* tmap, int mode, int num_sms, cudaStream_t st) {
-  switch (mode) {
-    case 0: return launch_t<BN, 0>(a, tmap, num_sms, st);
-    case 1: return launch_t<BN, 1>(a, tmap, num_sms, st);
-    case 2: return launch_t<BN, 2>(a, tmap, num_sms, st);
+cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int num_sms, cudaStream_t st) {
+  switch (g.mode) {
+    case 0: return launch_t<BN, 0>(a, g, mp, num_sms, st);
+    case 2: return launch_t<BN, 2>(a, g, mp, num_sms, st);
+    case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
+    case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -470,14 +646,53 @@ int conv_tc_pick_bn(int cout) {
   return cout % 256 == 0 ? 256 : 128;
 }
 
-cudaError_t conv_tc_launch(const ConvArgs& a, const CUtensorMap* tmap_b, int bn, int mode, int num_sms,
+int conv_tc_store_cols(int bn) { return bn < 64 ? bn : 64; }
+
+void conv_tc_spatial_tile(int OH, int OW, int N, int* wb, int* hb, int* nb) {
+  const int tiles_w = (OW + BM - 1) / BM;
+  *wb = (OW + tiles_w - 1) / tiles_w;
+  const int hmax = BM / *wb;
+  const int tiles_h = (OH + hmax - 1) / hmax;
+  *hb = (OH + tiles_h - 1) / tiles_h;
+  *nb = 1;
+  if (*hb == OH && tiles_w == 1) {
+    *nb = BM / (*wb * *hb);
+    if (*nb > N) *nb = N;
+    if (*nb < 1) *nb = 1;
+  }
+}
+
+cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mode, int wb, int hb, int nb, int num_sms,
                            cudaStream_t st) {
+  Geo g{};
+  g.mode = mode;
+  g.n_tiles = (a.Cout + bn - 1) / bn;
+  g.has_res = a.res != nullptr;
+  g.tma_out = !a.nchw;
+  if (mode == 4) {
+    g.wb = wb; g.hb = hb; g.nb = nb;
+    g.tiles_w = (a.OW + wb - 1) / wb;
+    g.tiles_h = (a.OH + hb - 1) / hb;
+    g.m_tiles = g.tiles_w * g.tiles_h * ((a.N + nb - 1) / nb);
+    g.cblocks = a.C / BK;
+    g.k_chunks = a.KH * a.KW * g.cblocks;
+    g.a_bytes = BK * 2 * wb * hb * nb;
+  } else {
+    g.m_tiles = (int)((a.M + BM - 1) / BM);
+    g.k_chunks = (a.K + BK - 1) / BK;
+    g.cblocks = a.C / BK;
+    g.a_bytes = A_STAGE_BYTES;
+  }
+  if ((mode == 3 || mode == 4) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
+  if (g.tma_out && !mp.y) return cudaErrorInvalidValue;
+  if (g.has_res && g.tma_out && !mp.r) return cudaErrorInvalidValue;
+  if (g.has_res && !g.tma_out) g.has_res = 0;  // NCHW path reads the residual directly
   switch (bn) {
-    case 32: return launch_mode<32>(a, tmap_b, mode, num_sms, st);
-    case 64: return launch_mode<64>(a, tmap_b, mode, num_sms, st);
-    case 128: return launch_mode<128>(a, tmap_b, mode, num_sms, st);
-    case 192: return launch_mode<192>(a, tmap_b, mode, num_sms, st);
-    case 256: return launch_mode<256>(a, tmap_b, mode, num_sms, st);
+    case 32: return launch_mode<32>(a, g, mp, num_sms, st);
+    case 64: return launch_mode<64>(a, g, mp, num_sms, st);
+    case 128: return launch_mode<128>(a, g, mp, num_sms, st);
+    case 192: return launch_mode<192>(a, g, mp, num_sms, st);
+    case 256: return launch_mode<256>(a, g, mp, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -32,21 +32,32 @@ struct ConvArgs {
   long long M;
 };
 
-// tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).
-//   mode 0: A gathered with 16-byte cp.async (C % 8 == 0)
-//   mode 1: A gathered with 8-byte cp.async (C == 4; the packed stem input)
-//   mode 2: A via registers with the bn-relu prologue (C % 8 == 0)
-// tmap_b: 2D tensor map over the packed [Cout][Kp] bf16 weights, box {64, bn}.
+// tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).  A-operand modes:
+//   0  cp.async 16-byte gather (C % 8 == 0): stems (space-to-depth / padded input)
+//   2  register gather with the bn-relu prologue (C % 8 == 0): DenseNet
+//   3  TMA 2D {64, 128} over the [M][C] matrix (1x1 stride-1 convs, linear layers)
+//   4  TMA 4D {64, wb*s, hb*s, nb} per filter tap over NHWC, traversal stride s
+// tmap_a: A tensor map (modes 3/4, else nullptr); tmap_b: 2D map over the packed
+// [Cout][Kp] bf16 weights with box {64, bn}.
+struct ConvMaps {
+  const CUtensorMap* a;  // A operand (modes 3/4) or nullptr
+  const CUtensorMap* b;  // weights
+  const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
+  const CUtensorMap* r;  // residual view or nullptr
+};
 int conv_tc_pick_bn(int cout);
-cudaError_t conv_tc_launch(const ConvArgs& a, const CUtensorMap* tmap_b, int bn, int mode,
+int conv_tc_store_cols(int bn);  // columns per epilogue TMA box (64, or bn if smaller)
+void conv_tc_spatial_tile(int OH, int OW, int N, int* wb, int* hb, int* nb);
+cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& maps, int bn, int mode, int wb, int hb, int nb,
                            int num_sms, cudaStream_t st);
 
 // SIMT fp32 path (weights packed [K][Cout] fp32).
 cudaError_t conv_simt_launch(const ConvArgs& a, cudaStream_t st);
 
-// NCHW fp32 images -> NHWC activations: fp32 with C=3 (is_bf16=0) or bf16 padded to C=4.
-cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int is_bf16,
-                              cudaStream_t st);
+// NCHW fp32 images -> NHWC activations.  layout 0: fp32, C=3.  layout 1: bf16, C=8
+// (channels 3..7 zero).  layout 2: bf16 space-to-depth 2x2 -> [N][H/2][W/2][16], channel
+// (a*2+b)*3+c holds pixel (2i+a, 2j+b) channel c, channels 12..15 zero.
+cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st);
 
 // Window pooling, NHWC -> NHWC.  mode 0 = max (-inf padding), 1 = avg (count k*k).
 struct PoolArgs {

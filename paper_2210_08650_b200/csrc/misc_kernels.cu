@@ -56,21 +56,55 @@ __device__ __forceinline__ void store_vec(T* p, const float (&f)[V]) {
   }
 }
 
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
 // ---------------------------------------------------------------- pack_input
-__global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int HW, int is_bf16) {
+__global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout) {
+  const int HW = H * W;
+  if (layout == 2) {
+    // space-to-depth 2x2: one thread per output pixel (n, i, j) of the (H/2) x (W/2) grid
+    const int H2 = H / 2, W2 = W / 2;
+    const long long total = (long long)N * H2 * W2;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+      const long long n = t / (H2 * W2);
+      const int rem = (int)(t - n * H2 * W2);
+      const int i = rem / W2, j = rem - (rem / W2) * W2;
+      float v[16];
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const float* src = img + n * 3 * HW + (long long)(2 * i + a) * W + (2 * j + b);
+#pragma unroll
+          for (int c = 0; c < 3; ++c) v[(a * 2 + b) * 3 + c] = __ldg(src + c * HW);
+        }
+#pragma unroll
+      for (int c = 12; c < 16; ++c) v[c] = 0.f;
+      uint4 o0, o1;
+      o0.x = pack2(v[0], v[1]); o0.y = pack2(v[2], v[3]); o0.z = pack2(v[4], v[5]); o0.w = pack2(v[6], v[7]);
+      o1.x = pack2(v[8], v[9]); o1.y = pack2(v[10], v[11]); o1.z = pack2(v[12], v[13]); o1.w = pack2(v[14], v[15]);
+      uint4* yo = reinterpret_cast<uint4*>(y) + t * 2;
+      yo[0] = o0;
+      yo[1] = o1;
+    }
+    return;
+  }
   const long long total = (long long)N * HW;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long n = i / HW;
     const long long p = i - n * HW;
     const float* src = img + n * 3 * HW + p;
     const float r = __ldg(src), g = __ldg(src + HW), b = __ldg(src + 2 * HW);
-    if (is_bf16) {
-      __nv_bfloat162 lo = __floats2bfloat162_rn(r, g);
-      __nv_bfloat162 hi = __floats2bfloat162_rn(b, 0.f);
-      uint2 o;
-      o.x = *reinterpret_cast<uint32_t*>(&lo);
-      o.y = *reinterpret_cast<uint32_t*>(&hi);
-      reinterpret_cast<uint2*>(y)[i] = o;
+    if (layout == 1) {
+      uint4 o;
+      o.x = pack2(r, g);
+      o.y = pack2(b, 0.f);
+      o.z = 0u;
+      o.w = 0u;
+      reinterpret_cast<uint4*>(y)[i] = o;
     } else {
       float* yo = static_cast<float*>(y) + i * 3;
       yo[0] = r; yo[1] = g; yo[2] = b;
@@ -199,9 +233,9 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 }  // namespace
 
-cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int is_bf16, cudaStream_t st) {
-  const long long total = (long long)N * H * W;
-  pack_input_kernel<<<grid_for(total, 256), 256, 0, st>>>(img, y, N, H * W, is_bf16);
+cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st) {
+  const long long total = layout == 2 ? (long long)N * (H / 2) * (W / 2) : (long long)N * H * W;
+  pack_input_kernel<<<grid_for(total, 256), 256, 0, st>>>(img, y, N, H, W, layout);
   return cudaGetLastError();
 }
 

@@ -93,6 +93,12 @@ struct Op {
   uint32_t kind = 0;             // plan_info kernel class
   double flops = 0, bytes = 0;   // per image
   std::string desc;              // human-readable (hapi_plan_describe)
+  int tc_mode = 0;               // conv_tc A-operand mode
+  int wb = 0, hb = 0, nb = 0;    // mode 4 spatial tile
+  int layout = 0;                // pack_in layout
+  CUtensorMap tmap_a;            // modes 3/4 (built after the arena is placed)
+  CUtensorMap tmap_y;            // NHWC output view (TMA-store epilogue)
+  CUtensorMap tmap_r;            // residual view
 };
 
 struct Buf {
@@ -198,11 +204,12 @@ struct ConvSpec {
   int cs = 0;            // stored channels per pixel of the input view (4 for the bf16 stem)
   int fh = 0, fw = 0;    // linear on a flattened (cin/(fh*fw), fh, fw) map: permute columns
   bool linear = false;
+  bool s2d = false;      // 7x7/s2/p3 stem re-expressed as 4x4/s1/p2 on a 2x2 space-to-depth input
 };
 
 hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   std::string key = s.wname + "|" + s.bname + "|" + s.fold_bn + "|" + s.pro_bn + "|" + std::to_string(s.cs) + "|" +
-                    std::to_string(s.fh) + "x" + std::to_string(s.fw);
+                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "");
   auto it = m->conv_index.find(key);
   if (it != m->conv_index.end()) {
     *out_idx = it->second;
@@ -222,13 +229,24 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   ConvW cw;
   cw.cs = s.cs;
   cw.cout = s.cout;
-  cw.kh = cw.kw = kk;
-  cw.stride = s.stride;
-  cw.pad = s.pad;
-  cw.K = kk * kk * s.cs;
+  cw.kh = cw.kw = s.s2d ? 4 : kk;
+  cw.stride = s.s2d ? 1 : s.stride;
+  cw.pad = s.s2d ? 2 : s.pad;
+  cw.K = cw.kh * cw.kw * s.cs;
   cw.real_flops_per_px = 2.0 * (double)kk * kk * s.cin * s.cout;
   // element (o, k) of the GEMM B operand, k ordered (r, s, c) over the stored input channels
   auto wval = [&](int o, int r, int t, int c) -> double {
+    if (s.s2d) {
+      // stored tap (r, t) of the 4x4 kernel, channel c = (a*2+b)*3 + ch of the 2x2 block:
+      // original tap (2r+a-1, 2t+b-1) of the 7x7 kernel (zero outside it)
+      if (c >= 12) return 0.0;
+      const int blk = c / 3, ch = c % 3, aa = blk / 2, bb = blk % 2;
+      const int orr = 2 * r + aa - 1, ott = 2 * t + bb - 1;
+      if (orr < 0 || orr >= kk || ott < 0 || ott >= kk) return 0.0;
+      double v = w[(((int64_t)o * s.cin + ch) * kk + orr) * kk + ott];
+      if (!fs.empty()) v *= fs[o];
+      return v;
+    }
     if (c >= s.cin) return 0.0;  // padded stored channel
     double v;
     if (s.linear) {
@@ -250,14 +268,15 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     if (!fs.empty()) bv = bv * fs[o] + fb[o];
     bias[o] = (float)bv;
   }
-  const int taps = kk * kk;
+  const int taps = cw.kh * cw.kw;
+  const int gk = cw.kw;
   if (m->bf16) {
     cw.Kp = (cw.K + 7) / 8 * 8;
     std::vector<uint16_t> hw((size_t)s.cout * cw.Kp, 0);
     for (int o = 0; o < s.cout; ++o)
       for (int tap = 0; tap < taps; ++tap)
         for (int c = 0; c < s.cs; ++c)
-          hw[(size_t)o * cw.Kp + tap * s.cs + c] = f2bf((float)wval(o, tap / kk, tap % kk, c));
+          hw[(size_t)o * cw.Kp + tap * s.cs + c] = f2bf((float)wval(o, tap / gk, tap % gk, c));
     uint16_t* dw;
     hapi_status st = upload(m, hw, &dw);
     if (st != HAPI_OK) return st;
@@ -279,7 +298,7 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     for (int o = 0; o < s.cout; ++o)
       for (int tap = 0; tap < taps; ++tap)
         for (int c = 0; c < s.cs; ++c)
-          hw[(size_t)(tap * s.cs + c) * s.cout + o] = (float)wval(o, tap / kk, tap % kk, c);
+          hw[(size_t)(tap * s.cs + c) * s.cout + o] = (float)wval(o, tap / gk, tap % gk, c);
     float* dw;
     hapi_status st = upload(m, hw, &dw);
     if (st != HAPI_OK) return st;
@@ -298,9 +317,9 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     if (st != HAPI_OK) return st;
     cw.mode = 2;
   } else {
-    cw.mode = (s.cs == 4 && m->bf16) ? 1 : 0;
+    cw.mode = 0;
   }
-  if (m->bf16 && cw.mode != 1 && s.cs % 8 != 0)
+  if (m->bf16 && s.cs % 8 != 0)
     return set_error(HAPI_ERR_UNSUPPORTED, "tensor-core conv needs C %% 8 == 0 (%s, C=%d)", s.wname.c_str(), s.cs);
   m->convs.push_back(cw);
   *out_idx = (int)m->convs.size() - 1;
@@ -338,13 +357,24 @@ struct Builder {
     if (res) { o.res = *res; o.has_res = true; }
     o.kind = m->bf16 ? 0 : 1;
     const ConvW& w = m->convs[ci];
+    if (m->bf16) {
+      o.tc_mode = w.mode;
+      if (w.mode == 0 && w.cs % 64 == 0) {
+        if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0) {
+          o.tc_mode = 3;
+        } else if (w.stride <= 2) {
+          conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
+          if (o.wb * w.stride <= 256 && o.hb * w.stride <= 256) o.tc_mode = 4;
+        }
+      }
+    }
     const double px = (double)out.H * out.W;
     o.flops = w.real_flops_per_px * px;
     o.bytes = ((double)in.H * in.W * (cs.linear ? in.C : cs.cin) + px * w.cout * (res ? 2 : 1)) * m->es;
     char d[256];
-    std::snprintf(d, sizeof(d), "%s %dx%d/s%d C%d->%d %dx%d->%dx%d bn%d mode%d%s%s%s", cs.wname.c_str(), w.kh, w.kw,
-                  w.stride, w.cs, w.cout, in.H, in.W, out.H, out.W, w.bn, w.mode, relu ? " relu" : "", res ? " +res" : "",
-                  cs.pro_bn.empty() ? "" : " prologue");
+    std::snprintf(d, sizeof(d), "%s %dx%d/s%d C%d->%d %dx%d->%dx%d bn%d mode%d%s%s%s%s", cs.wname.c_str(), w.kh, w.kw,
+                  w.stride, w.cs, w.cout, in.H, in.W, out.H, out.W, w.bn, o.tc_mode, relu ? " relu" : "",
+                  res ? " +res" : "", cs.pro_bn.empty() ? "" : " prologue", cs.s2d ? " s2d" : "");
     o.desc = d;
     emit(o);
     if (op_out) *op_out = &p.ops.back();
@@ -380,15 +410,21 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   b.p.split = split;
   const ArchDesc& A = *m->arch;
   const int H0 = (int)m->d.in_h, W0 = (int)m->d.in_w;
-  const int cs0 = m->bf16 ? 4 : 3;
-  // a1: pack the caller's NCHW fp32 images
-  View cur = b.compact(cs0, H0, W0);
+  // a1: pack the caller's NCHW fp32 images.  bf16: ResNet/DenseNet stems (7x7/s2/p3) read a
+  // 2x2 space-to-depth layout (16 channels at H/2 x W/2) so the stem gathers 16-byte pieces;
+  // other stems read the image padded to 8 channels.
+  const ModDesc& m0 = A.mods[0];
+  const bool s2d = m->bf16 && m0.kind == MK_CONV && m0.k == 7 && m0.stride == 2 && m0.pad == 3 && m0.cin == 3 &&
+                   H0 % 2 == 0 && W0 % 2 == 0;
+  const int layout = !m->bf16 ? 0 : (s2d ? 2 : 1);
+  View cur = layout == 2 ? b.compact(16, H0 / 2, W0 / 2) : b.compact(layout == 1 ? 8 : 3, H0, W0);
   {
     Op o;
     o.t = OP_PACK_IN;
     o.out = cur;
     o.kind = 3;
-    o.bytes = (double)H0 * W0 * (3 * 4 + cs0 * m->es);
+    o.layout = layout;
+    o.bytes = (double)H0 * W0 * 3 * 4 + (double)cur.C * cur.H * cur.W * m->es;
     b.emit(o);
   }
   const auto& mods = A.mods;
@@ -407,7 +443,9 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         cs.fold_bn = fold ? mods[i + 1].name : "";
         cs.cin = md.cin; cs.cout = md.cout; cs.k = md.k; cs.stride = md.stride; cs.pad = md.pad;
         cs.cs = cur.C;
-        View o = b.compact(md.cout, out_dim(cur.H, md.k, md.stride, md.pad), out_dim(cur.W, md.k, md.stride, md.pad));
+        cs.s2d = (i == 0 && s2d);
+        const int ih = cs.s2d ? H0 : cur.H, iw = cs.s2d ? W0 : cur.W;
+        View o = b.compact(md.cout, out_dim(ih, md.k, md.stride, md.pad), out_dim(iw, md.k, md.stride, md.pad));
         if ((st = b.conv(cs, cur, o, relu, nullptr)) != HAPI_OK) return st;
         cur = o;
         i = j + (relu ? 1 : 0);
@@ -689,7 +727,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
   const int isb = m->bf16 ? 1 : 0;
   switch (o.t) {
     case OP_PACK_IN:
-      e = pack_input_launch(images, vptr(m, p, o.out, out), nb, o.out.H, o.out.W, isb, st);
+      e = pack_input_launch(images, vptr(m, p, o.out, out), nb, (int)m->d.in_h, (int)m->d.in_w, o.layout, st);
       break;
     case OP_CONV: {
       const ConvW& w = m->convs[o.conv];
@@ -711,7 +749,16 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.relu = o.relu;
       a.nchw = o.nchw_out;
       a.M = (long long)nb * a.OH * a.OW;
-      e = m->bf16 ? conv_tc_launch(a, &w.tmap, w.bn, w.mode, m->num_sms, st) : conv_simt_launch(a, st);
+      if (m->bf16) {
+        ConvMaps mp;
+        mp.a = (o.tc_mode == 3 || o.tc_mode == 4) ? &o.tmap_a : nullptr;
+        mp.b = &w.tmap;
+        mp.y = o.nchw_out ? nullptr : &o.tmap_y;
+        mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
+        e = conv_tc_launch(a, mp, w.bn, o.tc_mode, o.wb, o.hb, o.nb, m->num_sms, st);
+      } else {
+        e = conv_simt_launch(a, st);
+      }
       break;
     }
     case OP_POOL: {
@@ -760,6 +807,82 @@ hapi_status run_chunk(hapi_model* m, const Plan& p, int nb, const float* images,
     if (s != HAPI_OK) return s;
   }
   if (evs) cudaEventRecord(evs[p.ops.size()], st);
+  return HAPI_OK;
+}
+
+// TMA descriptors of the A operand (modes 3/4) need the placed arena, so they are
+// encoded once after allocation.  The batch dimension spans max_batch images; smaller
+// calls read (and then discard) rows past the batch inside the same buffer.
+hapi_status encode_bf16(CUtensorMap* map, int rank, void* base, const cuuint64_t* dims, const cuuint64_t* strides,
+                        const cuuint32_t* box, const cuuint32_t* estr, CUtensorMapSwizzle swz, const std::string& what) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "tensor map encode failed (%d): %s", (int)r, what.c_str());
+  return HAPI_OK;
+}
+
+// Map over an NHWC activation view with the conv's tile geometry: 2D [M][C] with a
+// {cols, 128} box for linear tiles, 4D {C, W, H, N} with a {cols, wb, hb, nb} box for
+// mode-4 spatial tiles.  The batch extent is max_batch.
+hapi_status encode_view(hapi_model* m, const Plan& p, const Op& o, const View& v, int cols, CUtensorMap* map,
+                        const char* what) {
+  const cuuint64_t es = 2, ld = (cuuint64_t)v.ld;
+  const CUtensorMapSwizzle swz = cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  void* base = vptr(m, p, v, nullptr);
+  if (o.tc_mode == 4) {
+    cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)m->d.max_batch};
+    cuuint64_t strides[3] = {ld * es, ld * es * v.W, ld * es * v.W * v.H};
+    cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)o.wb, (cuuint32_t)o.hb, (cuuint32_t)o.nb};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return encode_bf16(map, 4, base, dims, strides, box, estr, swz, o.desc + " " + what);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)v.C, (cuuint64_t)m->d.max_batch * v.H * v.W};
+  cuuint64_t strides[1] = {ld * es};
+  cuuint32_t box[2] = {(cuuint32_t)cols, 128};
+  cuuint32_t estr[2] = {1, 1};
+  return encode_bf16(map, 2, base, dims, strides, box, estr, swz, o.desc + " " + what);
+}
+
+// TMA descriptors over arena views need the placed arena, so they are encoded once after
+// allocation.  The batch extent is max_batch; smaller calls touch rows past the batch
+// inside the same arena buffers only (never the caller's output, which is written by the
+// NCHW path).
+hapi_status finalize_tmaps(hapi_model* m) {
+  if (!m->bf16) return HAPI_OK;
+  for (Plan& p : m->plans) {
+    for (Op& o : p.ops) {
+      if (o.t != OP_CONV) continue;
+      const ConvW& w = m->convs[o.conv];
+      hapi_status st = HAPI_OK;
+      if (o.tc_mode == 3 || o.tc_mode == 4) {
+        void* base = vptr(m, p, o.in, nullptr);
+        const cuuint64_t es = 2, ld = (cuuint64_t)o.in.ld;
+        if (o.tc_mode == 3) {
+          cuuint64_t dims[2] = {(cuuint64_t)w.cs, (cuuint64_t)m->d.max_batch * o.in.H * o.in.W};
+          cuuint64_t strides[1] = {ld * es};
+          cuuint32_t box[2] = {64, 128};
+          cuuint32_t estr[2] = {1, 1};
+          st = encode_bf16(&o.tmap_a, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A");
+        } else {
+          const cuuint32_t sd = (cuuint32_t)w.stride;
+          cuuint64_t dims[4] = {(cuuint64_t)w.cs, (cuuint64_t)o.in.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+          cuuint64_t strides[3] = {ld * es, ld * es * o.in.W, ld * es * o.in.W * o.in.H};
+          cuuint32_t box[4] = {64, (cuuint32_t)o.wb * sd, (cuuint32_t)o.hb * sd, (cuuint32_t)o.nb};
+          cuuint32_t estr[4] = {1, sd, sd, 1};
+          st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A");
+        }
+        if (st != HAPI_OK) return st;
+      }
+      if (!o.nchw_out) {
+        const int cols = conv_tc_store_cols(w.bn);
+        if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y")) != HAPI_OK) return st;
+        if (o.has_res && (st = encode_view(m, p, o, o.res, cols, &o.tmap_r, "R")) != HAPI_OK) return st;
+      }
+    }
+  }
   return HAPI_OK;
 }
 
@@ -828,6 +951,7 @@ hapi_status hapi_model_create(const hapi_model_desc* desc, const float* const* p
   m->host_params.clear();
   {
     hapi_status st = dev_alloc(m.get(), (size_t)m->arena_bytes, &m->arena, false);
+    if (st == HAPI_OK) st = finalize_tmaps(m.get());
     if (st != HAPI_OK) {
       hapi_model_destroy(m.release());
       return st;
