@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
   constexpr bool TMA_A = (MODE == 3 || MODE == 4);
+  constexpr bool SPATIAL = (MODE == 4);
   const int S = g.stages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -297,15 +298,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
           const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
           int w0 = 0, h0 = 0, b0 = 0;
-          if (MODE == 4) {
+          if (SPATIAL) {
             tile_origin(g, tm, &w0, &h0, &b0);
             w0 = w0 * a.stride - a.pad;
             h0 = h0 * a.stride - a.pad;
           }
           for (int kc = 0; kc < g.k_chunks; ++kc) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], g.a_bytes + C::B_STAGE_BYTES);
             const uint32_t dA = smem_u32(sA + stage * A_STAGE_BYTES);
+            mbar_arrive_expect_tx(&full[stage], g.a_bytes + C::B_STAGE_BYTES);
             if (MODE == 3) {
               tma_load_2d(dA, &tmap_a, kc * BK, tm * BM, &full[stage]);
             } else {
@@ -436,7 +437,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint64_t bdesc = make_sdesc(smem_u32(sB + stage * C::B_STAGE_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
-            // advance 16 bf16 = 32 bytes along K inside the swizzle atom
+            // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle atom
             mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
           }
           mma_commit(&empty[stage]);
@@ -455,14 +456,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
         int w0 = 0, h0 = 0, b0 = 0;
-        if (MODE == 4) tile_origin(g, tm, &w0, &h0, &b0);
+        if (SPATIAL) tile_origin(g, tm, &w0, &h0, &b0);
         for (int jb = 0; jb < BN; jb += SB) {
           const int n0 = tn * BN + jb;
           if (n0 >= a.Cout) break;
           mbar_wait(&rempty[rs], rph ^ 1);
           mbar_arrive_expect_tx(&rfull[rs], g.res_box_bytes);
           const uint32_t dst = smem_u32(sR + rs * C::SB_BYTES);
-          if (MODE == 4)
+          if (SPATIAL)
             tma_load_4d(dst, &tmap_r, n0, w0, h0, b0, &rfull[rs]);
           else
             tma_load_2d(dst, &tmap_r, n0, tm * BM, &rfull[rs]);
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         epi_bar();
       } else {
         int w0 = 0, h0 = 0, b0 = 0;
-        if (MODE == 4) tile_origin(g, tm, &w0, &h0, &b0);
+        if (SPATIAL) tile_origin(g, tm, &w0, &h0, &b0);
         for (int jb = 0; jb < BN; jb += SB) {
           const int n0 = tn * BN + jb;
           if (n0 >= a.Cout) break;  // uniform
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           fence_proxy_async_smem();
           epi_bar();
           if (et == 0) {
-            if (MODE == 4)
+            if (SPATIAL)
               tma_store_4d(&tmap_y, stg, n0, w0, h0, b0);
             else
               tma_store_2d(&tmap_y, stg, n0, tm * BM);

@@ -55,8 +55,9 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& maps, int bn, int 
 cudaError_t conv_simt_launch(const ConvArgs& a, cudaStream_t st);
 
 // NCHW fp32 images -> NHWC activations.  layout 0: fp32, C=3.  layout 1: bf16, C=8
-// (channels 3..7 zero).  layout 2: bf16 space-to-depth 2x2 -> [N][H/2][W/2][16], channel
-// (a*2+b)*3+c holds pixel (2i+a, 2j+b) channel c, channels 12..15 zero.
+// (channels 3..7 zero).  layout 2: bf16 space-to-depth 2x2 with a zero border ->
+// [N][H/2+3][W/2+3][16]; padded pixel (i+2, j+2) channel (a*2+b)*3+c holds image pixel
+// (2i+a, 2j+b) channel c; channels 12..15 and the border are zero.
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st);
 
 // Window pooling, NHWC -> NHWC.  mode 0 = max (-inf padding), 1 = avg (count k*k).

@@ -65,24 +65,27 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 __global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout) {
   const int HW = H * W;
   if (layout == 2) {
-    // space-to-depth 2x2: one thread per output pixel (n, i, j) of the (H/2) x (W/2) grid
-    const int H2 = H / 2, W2 = W / 2;
-    const long long total = (long long)N * H2 * W2;
+    // space-to-depth 2x2 with a zero border (2 before, 1 after) so the stem's 4x4 window
+    // view never leaves the buffer: one thread per padded pixel of the (H/2+3) x (W/2+3) grid
+    const int H2 = H / 2, W2 = W / 2, HP = H2 + 3, WP = W2 + 3;
+    const long long total = (long long)N * HP * WP;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-      const long long n = t / (H2 * W2);
-      const int rem = (int)(t - n * H2 * W2);
-      const int i = rem / W2, j = rem - (rem / W2) * W2;
+      const long long n = t / (HP * WP);
+      const int rem = (int)(t - n * HP * WP);
+      const int i = rem / WP - 2, j = rem - (rem / WP) * WP - 2;
       float v[16];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int c = 0; c < 16; ++c) v[c] = 0.f;
+      if (i >= 0 && i < H2 && j >= 0 && j < W2) {
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-          const float* src = img + n * 3 * HW + (long long)(2 * i + a) * W + (2 * j + b);
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) v[(a * 2 + b) * 3 + c] = __ldg(src + c * HW);
-        }
+          for (int b = 0; b < 2; ++b) {
+            const float* src = img + n * 3 * HW + (long long)(2 * i + a) * W + (2 * j + b);
 #pragma unroll
-      for (int c = 12; c < 16; ++c) v[c] = 0.f;
+            for (int c = 0; c < 3; ++c) v[(a * 2 + b) * 3 + c] = __ldg(src + c * HW);
+          }
+      }
       uint4 o0, o1;
       o0.x = pack2(v[0], v[1]); o0.y = pack2(v[2], v[3]); o0.z = pack2(v[4], v[5]); o0.w = pack2(v[6], v[7]);
       o1.x = pack2(v[8], v[9]); o1.y = pack2(v[10], v[11]); o1.z = pack2(v[12], v[13]); o1.w = pack2(v[14], v[15]);
@@ -234,7 +237,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 }  // namespace
 
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st) {
-  const long long total = layout == 2 ? (long long)N * (H / 2) * (W / 2) : (long long)N * H * W;
+  const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * (W / 2 + 3) : (long long)N * H * W;
   pack_input_kernel<<<grid_for(total, 256), 256, 0, st>>>(img, y, N, H, W, layout);
   return cudaGetLastError();
 }

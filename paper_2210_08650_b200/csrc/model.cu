@@ -96,6 +96,7 @@ struct Op {
   int tc_mode = 0;               // conv_tc A-operand mode
   int wb = 0, hb = 0, nb = 0;    // mode 4 spatial tile
   int layout = 0;                // pack_in layout
+  bool s2d_view = false;         // stem over the padded space-to-depth window view
   CUtensorMap tmap_a;            // modes 3/4 (built after the arena is placed)
   CUtensorMap tmap_y;            // NHWC output view (TMA-store epilogue)
   CUtensorMap tmap_r;            // residual view
@@ -359,7 +360,13 @@ struct Builder {
     const ConvW& w = m->convs[ci];
     if (m->bf16) {
       o.tc_mode = w.mode;
-      if (w.mode == 0 && w.cs % 64 == 0) {
+      if (cs.s2d) {
+        // space-to-depth stem (4x4/s1 over 16-channel pixels): read as a window view whose
+        // rows are 4 adjacent padded pixels (128 B), W stride 32 B -> KH=4, KW=1, C=64 mode 4
+        conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
+        o.tc_mode = 4;
+        o.s2d_view = true;
+      } else if (w.mode == 0 && w.cs % 64 == 0) {
         if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0) {
           o.tc_mode = 3;
         } else if (w.stride <= 2) {
@@ -417,7 +424,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   const bool s2d = m->bf16 && m0.kind == MK_CONV && m0.k == 7 && m0.stride == 2 && m0.pad == 3 && m0.cin == 3 &&
                    H0 % 2 == 0 && W0 % 2 == 0;
   const int layout = !m->bf16 ? 0 : (s2d ? 2 : 1);
-  View cur = layout == 2 ? b.compact(16, H0 / 2, W0 / 2) : b.compact(layout == 1 ? 8 : 3, H0, W0);
+  View cur = layout == 2 ? b.compact(16, H0 / 2 + 3, W0 / 2 + 3) : b.compact(layout == 1 ? 8 : 3, H0, W0);
   {
     Op o;
     o.t = OP_PACK_IN;
@@ -749,9 +756,12 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.relu = o.relu;
       a.nchw = o.nchw_out;
       a.M = (long long)nb * a.OH * a.OW;
+      if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
+        a.C = 64; a.KH = 4; a.KW = 1; a.stride = 1; a.pad = 0;
+      }
       if (m->bf16) {
         ConvMaps mp;
-        mp.a = (o.tc_mode == 3 || o.tc_mode == 4) ? &o.tmap_a : nullptr;
+        mp.a = (o.tc_mode >= 3) ? &o.tmap_a : nullptr;
         mp.b = &w.tmap;
         mp.y = o.nchw_out ? nullptr : &o.tmap_y;
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
@@ -857,7 +867,18 @@ hapi_status finalize_tmaps(hapi_model* m) {
       if (o.t != OP_CONV) continue;
       const ConvW& w = m->convs[o.conv];
       hapi_status st = HAPI_OK;
-      if (o.tc_mode == 3 || o.tc_mode == 4) {
+      if (o.s2d_view) {
+        // overlapping window view of the padded s2d input: element (e, w, h, n) at
+        // base + n*HP*WP*32 + h*WP*32 + w*32 + 2e, e < 64 spans 4 adjacent pixels
+        void* base = vptr(m, p, o.in, nullptr);
+        const cuuint64_t px = (cuuint64_t)o.in.ld * 2;  // 32 B
+        cuuint64_t dims[4] = {64, (cuuint64_t)o.out.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+        cuuint64_t strides[3] = {px, px * o.in.W, px * o.in.W * o.in.H};
+        cuuint32_t box[4] = {64, (cuuint32_t)o.wb, (cuuint32_t)o.hb, (cuuint32_t)o.nb};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A");
+        if (st != HAPI_OK) return st;
+      } else if (o.tc_mode == 3 || o.tc_mode == 4) {
         void* base = vptr(m, p, o.in, nullptr);
         const cuuint64_t es = 2, ld = (cuuint64_t)o.in.ld;
         if (o.tc_mode == 3) {
