@@ -19,6 +19,8 @@ __global__ void __launch_bounds__(256)
   __shared__ float As[2][TK][TM + 4];
   __shared__ float Bs[2][TK][TN];
 
+  griddep_launch_dependents();
+  griddep_wait();
   const int tid = threadIdx.x;
   const long long m_base = (long long)blockIdx.x * TM;
   const int n_base = blockIdx.y * TN;
@@ -135,8 +137,7 @@ cudaError_t conv_simt_launch(const ConvArgs& a, cudaStream_t st) {
   const int nt = (a.Cout + TN - 1) / TN;
   if (mt <= 0 || nt <= 0) return cudaSuccess;
   dim3 grid((unsigned)mt, (unsigned)nt);
-  conv_simt_kernel<<<grid, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(conv_simt_kernel, grid, dim3(256), 0, st, a);
 }
 
 }  // namespace hapi

@@ -9,26 +9,29 @@
 //   GEMM view: D[M=N*OH*OW][Cout] = A[M][K] * B[Cout][K]^T, K = KH*KW*C ordered (r, s, c).
 //   A = activations (implicit im2col of NHWC), B = packed bf16 weights [Cout][Kp].
 //
-// Persistent, warp-specialized CTA (one per SM, 320 threads):
-//   warps 0-3  epilogue: thread = tile row (its TMEM lane).  Per 64-column block:
+// Persistent, warp-specialized CTA (one per SM, 448 threads):
+//   warps 0-7  epilogue: thread = tile row (its TMEM lane; two warps per lane quarter split
+//              the columns).  Per 64-column block:
 //              tcgen05.ld -> + bias (smem) + residual (swizzled smem block) -> ReLU ->
 //              bf16 into a 128B-swizzled staging block (conflict-free) -> one TMA store
 //              (2D [M][C] box, or the 4D spatial box of mode 4); NCHW send-buffer writes
 //              of the split layer go straight from registers (coalesced per channel)
-//   warps 4-7  producer.  A operand per K chunk (one filter tap x 64 channels):
+//   warps 8-11 producer.  A operand per K chunk (one filter tap x 64 channels):
 //                mode 3  TMA 2D box {64 ch, 128 rows} of the [M][C] matrix (1x1, stride 1)
 //                mode 4  TMA 4D box {64 ch, wb, hb, nb} of the NHWC tensor shifted by the tap
 //                        (traversal stride = conv stride; OOB zero fill = conv padding)
 //                mode 0  cp.async 16-byte gather (C % 8 == 0: stems)
 //                mode 2  register gather with the DenseNet bn-relu prologue
 //              B operand: TMA 2D box {64, BN} of the weights.  Both 128-byte swizzled.
-//   warp 8     TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
-//   warp 9     residual loader: TMA of the residual blocks into a 2-deep smem ring
+//   warp 12    TMEM allocator + tcgen05.mma issuer (one elected lane; M=128, N=BN, K=16)
+//   warp 13    residual loader: TMA of the residual blocks into a 2-deep smem ring
 // Pipelines: smem ring of STAGES (full/empty mbarriers, depth chosen per launch from the
 // smem left after the epilogue buffers), two TMEM accumulators (tfull/tempty) so the
 // epilogue of tile i overlaps the MMAs of tile i+1, residual ring (rfull/rempty), and
 // double-buffered TMA-store staging (bulk async-groups).
 #include <cuda_bf16.h>
+
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -37,15 +40,18 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;                 // 64 bf16 = one 128-byte swizzle atom row
-constexpr int NUM_EPI_WARPS = 4;
-constexpr int PROD_WARP0 = 4;
+constexpr int NUM_EPI_WARPS = 8;     // two per TMEM lane quarter, splitting the columns
+constexpr int NUM_EPI_THREADS = NUM_EPI_WARPS * 32;
+constexpr int PROD_WARP0 = 8;
 constexpr int NUM_PROD_THREADS = 128;
-constexpr int MMA_WARP = 8;
-constexpr int RES_WARP = 9;
-constexpr int NUM_THREADS = 10 * 32;
+constexpr int MMA_WARP = 12;
+constexpr int RES_WARP = 13;
+constexpr int NUM_THREADS = 14 * 32;
 constexpr int A_STAGE_BYTES = BM * BK * 2;
 constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in per CTA
 constexpr int MAX_STAGES = 8;
+constexpr int MAX_B_STAGES = 16;  // mode 6 weight ring
+constexpr int MAX_A_STAGES = 2;   // mode 6 halo ring
 
 // Static part of the shared-memory carve-up; the pipeline depth is chosen per launch.
 template <int BN>
@@ -58,6 +64,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 512 /*barriers*/;
+  static_assert((2 * MAX_B_STAGES + 2 * MAX_A_STAGES + 8) * 8 + 4 <= 512, "barrier area");
   static int stages(bool res) {
     int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
     return s > MAX_STAGES ? MAX_STAGES : s;
@@ -134,7 +141,19 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// One lane of a converged warp (the same lane every time) -> issue of tcgen05 / TMA ops
+// from warp-uniform code, so descriptors stay in uniform registers.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -147,6 +166,12 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
   d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
   d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
   return d;
+}
+// Row-shifted view into a 1024-aligned 128B-swizzled buffer, starting `row_off` rows in.
+// The MMA applies the 128B swizzle on absolute smem address bits (as TMA wrote it), so the
+// base-offset field stays 0 (measured on B200: encoding (addr >> 7) & 7 there corrupts it).
+__device__ __forceinline__ uint64_t make_sdesc_rows(uint32_t base, int row_off) {
+  return make_sdesc(base + (uint32_t)row_off * 128u);
 }
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
@@ -189,8 +214,11 @@ struct Geo {
   int wb, hb, nb;              // mode 4 spatial tile
   int tiles_w, tiles_h;        // mode 4
   int m_tiles, n_tiles, k_chunks, cblocks;
+  int k1_chunks;               // chunks of the first A source (the rest come from tmap_a2)
   int a_bytes;                 // TMA modes: bytes of one A box
-  int stages;                  // smem pipeline depth
+  int stages;                  // smem pipeline depth (A and B rings; mode 6: B ring)
+  int a_stages, a_stage_bytes; // mode 6: halo ring depth and slot size
+  int we;                      // mode 6: extended tile width (OW + KW - 1)
   int has_res;                 // residual tiles streamed by the loader warp
   int tma_out;                 // 1: epilogue writes via TMA store (NHWC views); 0: NCHW direct
   int res_box_bytes;           // bytes of one residual box
@@ -198,6 +226,13 @@ struct Geo {
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
 __device__ __forceinline__ long long row_to_m(const ConvArgs& a, const Geo& g, int tm, int i) {
+  if (g.mode == 6) {
+    const int h = i / g.we, w = i - (i / g.we) * g.we;
+    const int th = tm % g.tiles_h, n = tm / g.tiles_h;
+    const int oh = th * g.hb + h;
+    if (w >= a.OW || h >= g.hb || oh >= a.OH) return -1;
+    return ((long long)n * a.OH + oh) * a.OW + w;
+  }
   if (g.mode != 4) {
     const long long m = (long long)tm * BM + i;
     return m < a.M ? m : -1;
@@ -222,6 +257,13 @@ __device__ __forceinline__ void tile_origin(const Geo& g, int tm, int* w0, int* 
   *b0 = tb * g.nb;
 }
 
+// Row of the output box (staging / residual block) that tile row i lands in, or -1.
+__device__ __forceinline__ int staging_row(const Geo& g, int i, int OW) {
+  if (g.mode != 6) return i;
+  const int h = i / g.we, w = i - (i / g.we) * g.we;
+  return (w < OW && h < g.hb) ? h * OW + w : -1;
+}
+
 // Byte offset of 16-byte chunk `c` of row `r` inside a [rows x SWZ-byte] swizzled block.
 template <int SWZ>
 __device__ __forceinline__ uint32_t swz_off(int r, int c) {
@@ -234,22 +276,26 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const ConvArgs a, const Geo g, const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_y,
-                   const __grid_constant__ CUtensorMap tmap_r) {
+                   const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4);
-  constexpr bool SPATIAL = (MODE == 4);
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 6);
+  constexpr bool SPATIAL = (MODE == 4 || MODE == 6);
   const int S = g.stages;
+  const int AS = MODE == 6 ? g.a_stages : S;
+  const int ASZ = MODE == 6 ? g.a_stage_bytes : A_STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = sA + S * A_STAGE_BYTES;
+  uint8_t* sB = sA + AS * ASZ;
   uint8_t* sY = sB + S * C::B_STAGE_BYTES;                 // 2 output staging blocks
   uint8_t* sR = sY + 2 * C::SB_BYTES;                      // 2 residual blocks (if has_res)
   float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? 2 * C::SB_BYTES : 0));
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias + BN);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  uint64_t* empty = full + MAX_B_STAGES;
+  uint64_t* afull = empty + MAX_B_STAGES;    // mode 6 halo ring
+  uint64_t* aempty = afull + MAX_A_STAGES;
+  uint64_t* tfull = aempty + MAX_A_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
   uint64_t* rempty = rfull + 2;
@@ -257,17 +303,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  griddep_launch_dependents();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], TMA_A ? 1 : NUM_PROD_THREADS + 1);
       mbar_init(&empty[s], 1);
     }
+    for (int i = 0; i < MAX_A_STAGES; ++i) {
+      mbar_init(&afull[i], 1);
+      mbar_init(&aempty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], NUM_EPI_WARPS * 32);
+      mbar_init(&tempty[i], NUM_EPI_THREADS);
       mbar_init(&rfull[i], 1);
-      mbar_init(&rempty[i], NUM_EPI_WARPS * 32);
+      mbar_init(&rempty[i], NUM_EPI_THREADS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -285,6 +336,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  griddep_wait();  // the previous kernel's outputs are visible from here on
 
   const int num_tiles = g.m_tiles * g.n_tiles;
   const int OHW = a.OH * a.OW;
@@ -292,30 +344,72 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ producer
     const int pt = threadIdx.x - PROD_WARP0 * 32;
-    if (TMA_A) {
-      if (pt == 0) {
+    if (MODE == 6) {
+      // halo mode: one [(hb+KH-1) x we] pixel box per 64-channel block, then the taps' weights
+      if (warp == PROD_WARP0) {
+        uint32_t stage = 0, phase = 0, ast = 0, aph = 0;
+        const int taps = a.KH * a.KW;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+          const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+          int ow0, oh0, b0;
+          tile_origin(g, tm, &ow0, &oh0, &b0);
+          for (int cb = 0; cb < g.cblocks; ++cb) {
+            mbar_wait(&aempty[ast], aph ^ 1);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&afull[ast], g.a_bytes);
+              tma_load_4d(smem_u32(sA + ast * ASZ), &tmap_a, cb * BK, ow0 - a.pad, oh0 - a.pad, b0, &afull[ast]);
+            }
+            __syncwarp();
+            if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
+            for (int t = 0; t < taps; ++t) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              if (elect_one()) {
+                mbar_arrive_expect_tx(&full[stage], C::B_STAGE_BYTES);
+                tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, t * a.C + cb * BK, tn * BN, &full[stage]);
+              }
+              __syncwarp();
+              if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+            }
+          }
+        }
+      }
+    } else if (TMA_A) {
+      if (warp == PROD_WARP0) {
         uint32_t stage = 0, phase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
           const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
-          int w0 = 0, h0 = 0, b0 = 0;
+          int ow0 = 0, oh0 = 0, b0 = 0, w0 = 0, h0 = 0;
           if (SPATIAL) {
-            tile_origin(g, tm, &w0, &h0, &b0);
-            w0 = w0 * a.stride - a.pad;
-            h0 = h0 * a.stride - a.pad;
+            tile_origin(g, tm, &ow0, &oh0, &b0);
+            w0 = ow0 * a.stride - a.pad;
+            h0 = oh0 * a.stride - a.pad;
           }
+          int cb = 0, r = 0, sft = 0;  // (tap, channel block) of chunk kc, tracked incrementally
           for (int kc = 0; kc < g.k_chunks; ++kc) {
             mbar_wait(&empty[stage], phase ^ 1);
-            const uint32_t dA = smem_u32(sA + stage * A_STAGE_BYTES);
-            mbar_arrive_expect_tx(&full[stage], g.a_bytes + C::B_STAGE_BYTES);
-            if (MODE == 3) {
-              tma_load_2d(dA, &tmap_a, kc * BK, tm * BM, &full[stage]);
-            } else {
-              const int tap = kc / g.cblocks, cb = kc - tap * g.cblocks;
-              const int r = tap / a.KW, s = tap - r * a.KW;
-              tma_load_4d(dA, &tmap_a, cb * BK, w0 + s, h0 + r, b0, &full[stage]);
+            if (elect_one()) {
+              const uint32_t dA = smem_u32(sA + stage * A_STAGE_BYTES);
+              mbar_arrive_expect_tx(&full[stage], g.a_bytes + C::B_STAGE_BYTES);
+              if (kc >= g.k1_chunks) {
+                // fused downsample: 1x1 conv with stride2 over the block input
+                const int c2 = kc - g.k1_chunks;
+                if (MODE == 3)
+                  tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
+                else
+                  tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
+              } else if (MODE == 3) {
+                tma_load_2d(dA, &tmap_a, kc * BK, tm * BM, &full[stage]);
+              } else {
+                tma_load_4d(dA, &tmap_a, cb * BK, w0 + sft, h0 + r, b0, &full[stage]);
+              }
+              tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, kc * BK, tn * BN, &full[stage]);
             }
-            tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, kc * BK, tn * BN, &full[stage]);
+            __syncwarp();
             if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+            if (++cb == g.cblocks) {
+              cb = 0;
+              if (++sft == a.KW) { sft = 0; ++r; }
+            }
           }
         }
       }
@@ -418,11 +512,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == MMA_WARP) {
     // ================================================================ MMA issuer
-    if (lane == 0) {
+    // The whole warp runs the loop (waits, descriptor math in uniform registers); one
+    // elected lane issues the MMAs and their commits.
+    {
       // kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, M=128, N=BN
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                              ((uint32_t)(BM >> 4) << 24);
-      uint32_t stage = 0, phase = 0;
+      const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
+      uint32_t stage = 0, phase = 0, ast = 0, aph = 0;
       int iter = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
         const int acc = iter & 1;
@@ -430,18 +527,54 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        if (MODE == 6) {
+          // tap (r, s) reads the halo shifted by r*we + s rows (the extra we - OW columns per
+          // row are garbage rows of the tile, discarded by the epilogue)
+          const int taps = a.KH * a.KW;
+          uint32_t accum = 0;
+          for (int cb = 0; cb < g.cblocks; ++cb) {
+            mbar_wait(&afull[ast], aph);
+            tc_fence_after();
+            const uint32_t a_base = sA0 + ast * ASZ;
+            int r = 0, sft = 0;
+            for (int t = 0; t < taps; ++t) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint64_t adesc = make_sdesc_rows(a_base, r * g.we + sft);
+              const uint64_t bdesc = make_sdesc(sB0 + stage * C::B_STAGE_BYTES);
+              if (elect_one()) {
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum | k);
+                mma_commit(&empty[stage]);
+              }
+              __syncwarp();
+              accum = 1;
+              if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+              if (++sft == a.KW) { sft = 0; ++r; }
+            }
+            if (elect_one()) mma_commit(&aempty[ast]);
+            __syncwarp();
+            if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
+          }
+          if (elect_one()) mma_commit(&tfull[acc]);
+          __syncwarp();
+          continue;
+        }
         for (int kc = 0; kc < g.k_chunks; ++kc) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = make_sdesc(smem_u32(sA + stage * A_STAGE_BYTES));
-          const uint64_t bdesc = make_sdesc(smem_u32(sB + stage * C::B_STAGE_BYTES));
+          const uint64_t adesc = make_sdesc(sA0 + stage * A_STAGE_BYTES);
+          const uint64_t bdesc = make_sdesc(sB0 + stage * C::B_STAGE_BYTES);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle atom
-            mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
+            for (int k = 0; k < BK / 16; ++k) {
+              // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle atom
+              mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
+            }
+            mma_commit(&empty[stage]);
+            if (kc == g.k_chunks - 1) mma_commit(&tfull[acc]);
           }
-          mma_commit(&empty[stage]);
-          if (kc == g.k_chunks - 1) mma_commit(&tfull[acc]);
+          __syncwarp();
           if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
         }
       }
@@ -473,11 +606,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ================================================================ epilogue
-    // Thread = tile row (its TMEM lane).  Per SB-column block: TMEM -> registers, + bias
+    // Thread = tile row (its TMEM lane); warps w and w+4 share lane quarter w%4 and take
+    // alternate 32-column sub-chunks.  Per SB-column block: TMEM -> registers, + bias
     // (smem) + residual (TMA-prefetched swizzled smem block), ReLU, bf16 -> swizzled
     // staging block (conflict-free 16-byte stores) -> one TMA store per block.
-    const int row = warp * 32 + lane;
-    const int et = threadIdx.x;  // 0..127
+    const int quarter = warp & 3, gsel = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int srow = staging_row(g, row, a.OW);  // row of the TMA box this thread fills (-1: none)
+    const int et = threadIdx.x;  // 0..255
     __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.y);
     const __nv_bfloat16* rb = static_cast<const __nv_bfloat16*>(a.res);
     uint32_t rs = 0, rph = 0;
@@ -489,13 +625,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t acc_phase = (iter >> 1) & 1;
       // bias of this tile's columns -> smem (the previous tile's readers are past the
       // last epi_bar of that tile)
-      for (int j = et; j < BN; j += 128) {
+      for (int j = et; j < BN; j += NUM_EPI_THREADS) {
         const int n = tn * BN + j;
         sBias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((uint32_t)(warp * 32) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       if (!g.tma_out) {
         // final layer straight into the NCHW send buffer (consecutive rows = consecutive
         // pixels, so thread-per-row stores are coalesced per channel)
@@ -507,7 +643,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           pix = (int)(m - (long long)img * OHW);
         }
 #pragma unroll 1
-        for (int j0 = 0; j0 < BN; j0 += 32) {
+        for (int j0 = gsel * 32; j0 < BN; j0 += 64) {
           uint32_t v[32];
           tmem_ld32(t_row + j0, v);
           tmem_wait_ld();
@@ -540,7 +676,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (g.has_res) mbar_wait(&rfull[rs], rph);
           const uint32_t rsm = smem_u32(sR + rs * C::SB_BYTES);
 #pragma unroll
-          for (int sub = 0; sub < SB / 32; ++sub) {
+          for (int sub = gsel; sub < SB / 32; sub += 2) {
             uint32_t v[32];
             tmem_ld32(t_row + jb + sub * 32, v);
             tmem_wait_ld();
@@ -550,11 +686,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               float f[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c4 * 8 + j]) + sBias[jb + chunk * 8 + j];
+              if (srow < 0) continue;
               if (g.has_res) {
                 uint32_t r0, r1, r2, r3;
                 asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-                             : "r"(rsm + swz_off<C::SWZ>(row, chunk)));
+                             : "r"(rsm + swz_off<C::SWZ>(srow, chunk)));
                 const uint32_t rr[4] = {r0, r1, r2, r3};
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -567,7 +704,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
               }
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + swz_off<C::SWZ>(row, chunk)),
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + swz_off<C::SWZ>(srow, chunk)),
                            "r"(pack_bf16x2(f[0], f[1])), "r"(pack_bf16x2(f[2], f[3])), "r"(pack_bf16x2(f[4], f[5])),
                            "r"(pack_bf16x2(f[6], f[7]))
                            : "memory");
@@ -614,16 +751,24 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  g.stages = C::stages(g.has_res);
-  g.res_box_bytes = g.mode == 4 ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
-  const int smem = C::smem_bytes(g.stages, g.has_res);
+  g.res_box_bytes = (g.mode == 4 || g.mode == 6) ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
+  int smem;
+  if (g.mode == 6) {
+    const int rest = SMEM_LIMIT - C::FIXED - (g.has_res ? 2 * C::SB_BYTES : 0) - g.a_stages * g.a_stage_bytes;
+    g.stages = rest / C::B_STAGE_BYTES;
+    if (g.stages > MAX_B_STAGES) g.stages = MAX_B_STAGES;
+    if (g.stages < 2) return cudaErrorInvalidValue;
+    smem = g.a_stages * g.a_stage_bytes + g.stages * C::B_STAGE_BYTES + C::FIXED + (g.has_res ? 2 * C::SB_BYTES : 0);
+  } else {
+    g.stages = C::stages(g.has_res);
+    smem = C::smem_bytes(g.stages, g.has_res);
+  }
   const int tiles = g.m_tiles * g.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
   const CUtensorMap* b = mp.b;
-  conv_tc_kernel<BN, MODE><<<grid, NUM_THREADS, smem, st>>>(a, g, mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b,
-                                                            mp.r ? *mp.r : *b);
-  return cudaGetLastError();
+  return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
+                    mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b);
 }
 
 template <int BN>
@@ -633,6 +778,7 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 2: return launch_t<BN, 2>(a, g, mp, num_sms, st);
     case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
+    case 6: return launch_t<BN, 6>(a, g, mp, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -670,7 +816,22 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   g.n_tiles = (a.Cout + bn - 1) / bn;
   g.has_res = a.res != nullptr;
   g.tma_out = !a.nchw;
-  if (mode == 4) {
+  if (mode == 6) {
+    // halo tile: full output rows (wb = OW), hb rows, one image; extended width we = OW + KW - 1
+    if (a.stride != 1 || a.C % BK != 0) return cudaErrorInvalidValue;
+    g.we = a.OW + a.KW - 1;
+    g.wb = a.OW; g.hb = hb; g.nb = 1;
+    g.tiles_w = 1;
+    g.tiles_h = (a.OH + hb - 1) / hb;
+    g.m_tiles = g.tiles_h * a.N;
+    g.cblocks = a.C / BK;
+    g.k_chunks = a.KH * a.KW * g.cblocks;
+    g.a_bytes = BK * 2 * g.we * (hb + a.KH - 1);
+    const int rows_read = (a.KH - 1) * g.we + (a.KW - 1) + BM;   // by the last tap's MMA
+    const int rows = rows_read > g.a_bytes / 128 ? rows_read : g.a_bytes / 128;
+    g.a_stage_bytes = (rows * 128 + 1023) / 1024 * 1024;
+    g.a_stages = MAX_A_STAGES;
+  } else if (mode == 4) {
     g.wb = wb; g.hb = hb; g.nb = nb;
     g.tiles_w = (a.OW + wb - 1) / wb;
     g.tiles_h = (a.OH + hb - 1) / hb;
@@ -684,7 +845,12 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     g.cblocks = a.C / BK;
     g.a_bytes = A_STAGE_BYTES;
   }
-  if ((mode == 3 || mode == 4) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
+  g.k1_chunks = g.k_chunks;
+  if (a.k2_chunks > 0) {
+    if ((mode != 3 && mode != 4) || !mp.a2) return cudaErrorInvalidValue;
+    g.k_chunks += a.k2_chunks;
+  }
+  if ((mode == 3 || mode == 4 || mode == 6) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
   if (g.tma_out && !mp.y) return cudaErrorInvalidValue;
   if (g.has_res && g.tma_out && !mp.r) return cudaErrorInvalidValue;
   if (g.has_res && !g.tma_out) g.has_res = 0;  // NCHW path reads the residual directly

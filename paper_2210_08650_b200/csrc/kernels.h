@@ -7,8 +7,44 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 
 namespace hapi {
+
+// Programmatic dependent launch: every kernel of the plan is launched with the PDL
+// attribute, calls griddep_launch_dependents() early and griddep_wait() before its first
+// global-memory access, so its prologue (barrier init, TMEM alloc, descriptor prefetch)
+// overlaps the previous kernel's tail.  HAPI_PDL=0 disables it.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#endif
 
 // Implicit-GEMM convolution: M = N*OH*OW output pixels, N = Cout, K = KH*KW*C.
 struct ConvArgs {
@@ -30,6 +66,11 @@ struct ConvArgs {
   int relu;             // apply ReLU after bias/residual
   int nchw;             // 1: y is contiguous NCHW [N][Cout][OH][OW]
   long long M;
+  // optional second A source, K-concatenated after the first (a ResNet downsample 1x1 conv
+  // fused into the block's last conv): k2_chunks 64-channel chunks of a 1x1 conv with
+  // stride `stride2` over its own input (TMA modes only)
+  int k2_chunks;
+  int stride2;
 };
 
 // tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).  A-operand modes:
@@ -41,6 +82,7 @@ struct ConvArgs {
 // [Cout][Kp] bf16 weights with box {64, bn}.
 struct ConvMaps {
   const CUtensorMap* a;  // A operand (modes 3/4) or nullptr
+  const CUtensorMap* a2; // second A source (k2_chunks > 0) or nullptr
   const CUtensorMap* b;  // weights
   const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
   const CUtensorMap* r;  // residual view or nullptr

@@ -63,6 +63,8 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 
 // ---------------------------------------------------------------- pack_input
 __global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int HW = H * W;
   if (layout == 2) {
     // space-to-depth 2x2 with a zero border (2 before, 1 after) so the stem's 4x4 window
@@ -118,6 +120,8 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
 // ---------------------------------------------------------------- pooling
 template <typename T, int V>
 __global__ void pool_kernel(const PoolArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int cg = a.C / V;
   const long long total = (long long)a.N * a.OH * a.OW * cg;
   const T* x = static_cast<const T*>(a.x);
@@ -154,6 +158,8 @@ __global__ void pool_kernel(const PoolArgs a) {
 
 template <typename T, int V>
 __global__ void adaptive_kernel(const AdaptiveArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int cg = a.C / V;
   const long long total = (long long)a.N * a.OH * a.OW * cg;
   const T* x = static_cast<const T*>(a.x);
@@ -186,6 +192,8 @@ __global__ void adaptive_kernel(const AdaptiveArgs a) {
 
 template <typename T, int V>
 __global__ void bn_act_kernel(const EltArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int cg = a.C / V;
   const long long total = (long long)a.N * a.HW * cg;
   const T* x = static_cast<const T*>(a.x);
@@ -209,6 +217,8 @@ __global__ void bn_act_kernel(const EltArgs a) {
 // NHWC (ld) -> NCHW through a 32x32 shared-memory tile: coalesced on both sides.
 template <typename T>
 __global__ void pack_output_kernel(const T* __restrict__ x, int HW, int C, int x_ld, T* __restrict__ y) {
+  griddep_launch_dependents();
+  griddep_wait();
   __shared__ T tile[32][33];
   const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
   const long long n = blockIdx.z;
@@ -238,7 +248,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st) {
   const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * (W / 2 + 3) : (long long)N * H * W;
-  pack_input_kernel<<<grid_for(total, 256), 256, 0, st>>>(img, y, N, H, W, layout);
+  launch_pdl(pack_input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, img, y, N, H, W, layout);
   return cudaGetLastError();
 }
 
@@ -246,14 +256,14 @@ cudaError_t pool_launch(const PoolArgs& a, int is_bf16, cudaStream_t st) {
   const long long pix = (long long)a.N * a.OH * a.OW;
   if (is_bf16) {
     if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
-      pool_kernel<__nv_bfloat16, 8><<<grid_for(pix * (a.C / 8), 256), 256, 0, st>>>(a);
+      launch_pdl(pool_kernel<__nv_bfloat16, 8>, dim3(grid_for(pix * (a.C / 8), 256)), dim3(256), 0, st, a);
     else
-      pool_kernel<__nv_bfloat16, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+      launch_pdl(pool_kernel<__nv_bfloat16, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);
   } else {
     if (a.C % 4 == 0 && a.x_ld % 4 == 0 && a.y_ld % 4 == 0 && aligned16(a.x) && aligned16(a.y))
-      pool_kernel<float, 4><<<grid_for(pix * (a.C / 4), 256), 256, 0, st>>>(a);
+      launch_pdl(pool_kernel<float, 4>, dim3(grid_for(pix * (a.C / 4), 256)), dim3(256), 0, st, a);
     else
-      pool_kernel<float, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+      launch_pdl(pool_kernel<float, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);
   }
   return cudaGetLastError();
 }
@@ -262,14 +272,14 @@ cudaError_t adaptive_avgpool_launch(const AdaptiveArgs& a, int is_bf16, cudaStre
   const long long pix = (long long)a.N * a.OH * a.OW;
   if (is_bf16) {
     if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
-      adaptive_kernel<__nv_bfloat16, 8><<<grid_for(pix * (a.C / 8), 256), 256, 0, st>>>(a);
+      launch_pdl(adaptive_kernel<__nv_bfloat16, 8>, dim3(grid_for(pix * (a.C / 8), 256)), dim3(256), 0, st, a);
     else
-      adaptive_kernel<__nv_bfloat16, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+      launch_pdl(adaptive_kernel<__nv_bfloat16, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);
   } else {
     if (a.C % 4 == 0 && a.x_ld % 4 == 0 && a.y_ld % 4 == 0 && aligned16(a.x) && aligned16(a.y))
-      adaptive_kernel<float, 4><<<grid_for(pix * (a.C / 4), 256), 256, 0, st>>>(a);
+      launch_pdl(adaptive_kernel<float, 4>, dim3(grid_for(pix * (a.C / 4), 256)), dim3(256), 0, st, a);
     else
-      adaptive_kernel<float, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+      launch_pdl(adaptive_kernel<float, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);
   }
   return cudaGetLastError();
 }
@@ -278,14 +288,14 @@ cudaError_t bn_act_launch(const EltArgs& a, int is_bf16, cudaStream_t st) {
   const long long pix = (long long)a.N * a.HW;
   if (is_bf16) {
     if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
-      bn_act_kernel<__nv_bfloat16, 8><<<grid_for(pix * (a.C / 8), 256), 256, 0, st>>>(a);
+      launch_pdl(bn_act_kernel<__nv_bfloat16, 8>, dim3(grid_for(pix * (a.C / 8), 256)), dim3(256), 0, st, a);
     else
-      bn_act_kernel<__nv_bfloat16, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+      launch_pdl(bn_act_kernel<__nv_bfloat16, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);
   } else {
     if (a.C % 4 == 0 && a.x_ld % 4 == 0 && a.y_ld % 4 == 0 && aligned16(a.x) && aligned16(a.y))
-      bn_act_kernel<float, 4><<<grid_for(pix * (a.C / 4), 256), 256, 0, st>>>(a);
+      launch_pdl(bn_act_kernel<float, 4>, dim3(grid_for(pix * (a.C / 4), 256)), dim3(256), 0, st, a);
     else
-      bn_act_kernel<float, 1><<<grid_for(pix * a.C, 256), 256, 0, st>>>(a);
+      launch_pdl(bn_act_kernel<float, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);
   }
   return cudaGetLastError();
 }
@@ -297,10 +307,10 @@ cudaError_t pack_output_launch(const void* x, int N, int HW, int C, int x_ld, vo
   }
   dim3 grid((HW + 31) / 32, (C + 31) / 32, N), block(32, 8);
   if (is_bf16)
-    pack_output_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(static_cast<const __nv_bfloat16*>(x), HW, C, x_ld,
+    launch_pdl(pack_output_kernel<__nv_bfloat16>, dim3(grid), dim3(block), 0, st, static_cast<const __nv_bfloat16*>(x), HW, C, x_ld,
                                                              static_cast<__nv_bfloat16*>(y));
   else
-    pack_output_kernel<float><<<grid, block, 0, st>>>(static_cast<const float*>(x), HW, C, x_ld, static_cast<float*>(y));
+    launch_pdl(pack_output_kernel<float>, dim3(grid), dim3(block), 0, st, static_cast<const float*>(x), HW, C, x_ld, static_cast<float*>(y));
   return cudaGetLastError();
 }
 

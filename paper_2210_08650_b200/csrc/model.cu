@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -61,6 +62,22 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+bool halo_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_HALO");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool fused_ds_disabled() {
+  static const bool off = [] {
+    const char* e = std::getenv("HAPI_FUSE_DS");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 // ---------------------------------------------------------------- model structures
 struct ConvW {
   int cs = 0;        // channels per pixel consumed (stored)
@@ -73,6 +90,7 @@ struct ConvW {
   CUtensorMap tmap;
   int bn = 0, mode = 0;
   double real_flops_per_px = 0;  // 2 * K_real * Cout
+  int K2 = 0, cs2 = 0, stride2 = 1;  // fused downsample source (bf16): 1x1/stride2 over cs2 channels
 };
 
 enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT };
@@ -100,6 +118,9 @@ struct Op {
   CUtensorMap tmap_a;            // modes 3/4 (built after the arena is placed)
   CUtensorMap tmap_y;            // NHWC output view (TMA-store epilogue)
   CUtensorMap tmap_r;            // residual view
+  bool dual = false;             // second A source (fused downsample) = in2
+  View in2;
+  CUtensorMap tmap_a2;
 };
 
 struct Buf {
@@ -141,6 +162,16 @@ struct hapi_model {
   int64_t stage_out_bytes = 0;
   cudaEvent_t ev[8] = {};
   bool host_ready = false;
+  // CUDA graphs of one chunk's launch sequence, keyed by (split, batch, images, out)
+  struct GraphEntry {
+    uint32_t split;
+    int nb;
+    const void* images;
+    void* out;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;
 };
 
 namespace {
@@ -206,11 +237,16 @@ struct ConvSpec {
   int fh = 0, fw = 0;    // linear on a flattened (cin/(fh*fw), fh, fw) map: permute columns
   bool linear = false;
   bool s2d = false;      // 7x7/s2/p3 stem re-expressed as 4x4/s1/p2 on a 2x2 space-to-depth input
+  // fused downsample (bf16): out = conv(x1) + ds(x2) with ds a 1x1/stride2 conv + folded BN,
+  // packed as extra K columns after the first conv's
+  std::string w2name, fold2;
+  int cin2 = 0, stride2 = 1;
 };
 
 hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   std::string key = s.wname + "|" + s.bname + "|" + s.fold_bn + "|" + s.pro_bn + "|" + std::to_string(s.cs) + "|" +
-                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "");
+                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "") + "|" + s.w2name + "|" +
+                    s.fold2;
   auto it = m->conv_index.find(key);
   if (it != m->conv_index.end()) {
     *out_idx = it->second;
@@ -226,6 +262,14 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   std::vector<double> fs, fb;
   if (!s.fold_bn.empty() && !bn_affine(m, s.fold_bn, s.cout, fs, fb))
     return set_error(HAPI_ERR_INVALID_MODEL, "bn %s missing", s.fold_bn.c_str());
+  const float* w2 = nullptr;
+  std::vector<double> fs2, fb2;
+  if (!s.w2name.empty()) {
+    if (!m->bf16) return set_error(HAPI_ERR_UNSUPPORTED, "fused downsample is a bf16-path feature");
+    if (!(w2 = P(m, s.w2name, (int64_t)s.cout * s.cin2)))
+      return set_error(HAPI_ERR_INVALID_MODEL, "param %s missing or wrong shape", s.w2name.c_str());
+    if (!bn_affine(m, s.fold2, s.cout, fs2, fb2)) return set_error(HAPI_ERR_INVALID_MODEL, "bn %s missing", s.fold2.c_str());
+  }
 
   ConvW cw;
   cw.cs = s.cs;
@@ -234,7 +278,10 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   cw.stride = s.s2d ? 1 : s.stride;
   cw.pad = s.s2d ? 2 : s.pad;
   cw.K = cw.kh * cw.kw * s.cs;
-  cw.real_flops_per_px = 2.0 * (double)kk * kk * s.cin * s.cout;
+  cw.real_flops_per_px = 2.0 * ((double)kk * kk * s.cin + s.cin2) * s.cout;
+  cw.K2 = w2 ? s.cin2 : 0;
+  cw.cs2 = s.cin2;
+  cw.stride2 = s.stride2;
   // element (o, k) of the GEMM B operand, k ordered (r, s, c) over the stored input channels
   auto wval = [&](int o, int r, int t, int c) -> double {
     if (s.s2d) {
@@ -267,17 +314,22 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   for (int o = 0; o < s.cout; ++o) {
     double bv = b0 ? (double)b0[o] : 0.0;
     if (!fs.empty()) bv = bv * fs[o] + fb[o];
+    if (w2) bv += fb2[o];
     bias[o] = (float)bv;
   }
   const int taps = cw.kh * cw.kw;
   const int gk = cw.kw;
   if (m->bf16) {
-    cw.Kp = (cw.K + 7) / 8 * 8;
+    if (w2 && cw.K % 64 != 0) return set_error(HAPI_ERR_UNSUPPORTED, "fused downsample needs K1 %% 64 == 0");
+    cw.Kp = (cw.K + cw.K2 + 7) / 8 * 8;
     std::vector<uint16_t> hw((size_t)s.cout * cw.Kp, 0);
-    for (int o = 0; o < s.cout; ++o)
+    for (int o = 0; o < s.cout; ++o) {
       for (int tap = 0; tap < taps; ++tap)
         for (int c = 0; c < s.cs; ++c)
           hw[(size_t)o * cw.Kp + tap * s.cs + c] = f2bf((float)wval(o, tap / gk, tap % gk, c));
+      for (int c = 0; c < cw.K2; ++c)
+        hw[(size_t)o * cw.Kp + cw.K + c] = f2bf((float)((double)w2[(int64_t)o * s.cin2 + c] * fs2[o]));
+    }
     uint16_t* dw;
     hapi_status st = upload(m, hw, &dw);
     if (st != HAPI_OK) return st;
@@ -348,7 +400,8 @@ struct Builder {
     p.ops.push_back(o);
     return p.ops.back();
   }
-  hapi_status conv(const ConvSpec& cs, const View& in, const View& out, bool relu, const View* res, Op** op_out = nullptr) {
+  hapi_status conv(const ConvSpec& cs, const View& in, const View& out, bool relu, const View* res, Op** op_out = nullptr,
+                   const View* in2 = nullptr) {
     int ci;
     hapi_status st = make_conv(m, cs, &ci);
     if (st != HAPI_OK) return st;
@@ -356,19 +409,39 @@ struct Builder {
     o.t = OP_CONV;
     o.in = in; o.out = out; o.conv = ci; o.relu = relu;
     if (res) { o.res = *res; o.has_res = true; }
+    if (in2) { o.in2 = *in2; o.dual = true; }
     o.kind = m->bf16 ? 0 : 1;
     const ConvW& w = m->convs[ci];
     if (m->bf16) {
       o.tc_mode = w.mode;
-      if (cs.s2d) {
+      if (in2) {
+        // fused downsample: both A sources must produce rows in the same order
+        if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0 && cs.stride2 == 1) {
+          o.tc_mode = 3;
+        } else {
+          conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
+          o.tc_mode = 4;
+        }
+      } else if (cs.s2d) {
         // space-to-depth stem (4x4/s1 over 16-channel pixels): read as a window view whose
         // rows are 4 adjacent padded pixels (128 B), W stride 32 B -> KH=4, KW=1, C=64 mode 4
         conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
         o.tc_mode = 4;
         o.s2d_view = true;
       } else if (w.mode == 0 && w.cs % 64 == 0) {
+        const int we = out.W + w.kw - 1;
         if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0) {
           o.tc_mode = 3;
+        } else if (w.stride == 1 && w.kh > 1 && we <= 128 && halo_enabled() &&
+                   out.W * ((out.H + ((out.H + 128 / we - 1) / (128 / we)) - 1) / ((out.H + 128 / we - 1) / (128 / we))) >= 96) {
+          // halo mode: one input box per 64-channel block, taps from row-shifted descriptors
+          // (only when a tile keeps >= 96 of its 128 rows valid; 7x7 maps use mode 4)
+          const int hmax = 128 / we;
+          const int tiles_h = (out.H + hmax - 1) / hmax;
+          o.hb = (out.H + tiles_h - 1) / tiles_h;
+          o.wb = out.W;
+          o.nb = 1;
+          o.tc_mode = 6;
         } else if (w.stride <= 2) {
           conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
           if (o.wb * w.stride <= 256 && o.hb * w.stride <= 256) o.tc_mode = 4;
@@ -377,11 +450,13 @@ struct Builder {
     }
     const double px = (double)out.H * out.W;
     o.flops = w.real_flops_per_px * px;
-    o.bytes = ((double)in.H * in.W * (cs.linear ? in.C : cs.cin) + px * w.cout * (res ? 2 : 1)) * m->es;
+    o.bytes = ((double)in.H * in.W * (cs.linear ? in.C : cs.cin) + px * w.cout * (res ? 2 : 1) +
+               (in2 ? (double)in2->H * in2->W * in2->C : 0.0)) * m->es;
     char d[256];
-    std::snprintf(d, sizeof(d), "%s %dx%d/s%d C%d->%d %dx%d->%dx%d bn%d mode%d%s%s%s%s", cs.wname.c_str(), w.kh, w.kw,
-                  w.stride, w.cs, w.cout, in.H, in.W, out.H, out.W, w.bn, o.tc_mode, relu ? " relu" : "",
-                  res ? " +res" : "", cs.pro_bn.empty() ? "" : " prologue", cs.s2d ? " s2d" : "");
+    std::snprintf(d, sizeof(d), "%s %dx%d/s%d C%d->%d %dx%d->%dx%d bn%d mode%d%s%s%s%s%s", cs.wname.c_str(), w.kh,
+                  w.kw, w.stride, w.cs, w.cout, in.H, in.W, out.H, out.W, w.bn, o.tc_mode, relu ? " relu" : "",
+                  res ? " +res" : "", cs.pro_bn.empty() ? "" : " prologue", cs.s2d ? " s2d" : "",
+                  in2 ? " +fused-downsample" : "");
     o.desc = d;
     emit(o);
     if (op_out) *op_out = &p.ops.back();
@@ -407,6 +482,7 @@ bool is_fresh_output(const Plan& p, int buf) {
   for (const Op& o : p.ops) {
     if (o.in.buf == buf && o.t != OP_PACK_IN) ++refs;
     if (o.has_res && o.res.buf == buf) ++refs;
+    if (o.dual && o.in2.buf == buf) ++refs;
     if (o.out.buf == buf) ++refs;
   }
   return refs == 1 && !p.ops.empty() && p.ops.back().out.buf == buf;
@@ -588,8 +664,10 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           c1.cin = md.cin; c1.cout = md.planes; c1.k = 3; c1.stride = md.stride; c1.pad = 1; c1.cs = x.C;
           if ((st = b.conv(c1, x, t, true, nullptr)) != HAPI_OK) return st;
         }
+        // bf16: the downsample 1x1 joins the last conv as a second K-concatenated A source
+        const bool fuse_ds = md.ds && m->bf16 && x.C % 64 == 0 && md.planes % 64 == 0 && !fused_ds_disabled();
         View idn = x;
-        if (md.ds) {
+        if (md.ds && !fuse_ds) {
           idn = b.compact(md.cout, OH, OW);
           ConvSpec cd;
           cd.wname = p + ".downsample.0.weight"; cd.fold_bn = p + ".downsample.1";
@@ -604,9 +682,20 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           cl.wname = p + ".conv2.weight"; cl.fold_bn = p + ".bn2";
           cl.cin = md.planes; cl.cout = md.cout; cl.k = 3; cl.pad = 1; cl.cs = md.planes;
         }
-        // out = relu(bn(conv(t)) + idn), written in place over idn
-        if ((st = b.conv(cl, t, idn, true, &idn)) != HAPI_OK) return st;
-        cur = idn;
+        if (fuse_ds) {
+          // out = relu(bn(conv(t)) + bn_ds(conv1x1_s(x))) in one GEMM, into a fresh buffer
+          cl.w2name = p + ".downsample.0.weight";
+          cl.fold2 = p + ".downsample.1";
+          cl.cin2 = md.cin;
+          cl.stride2 = md.stride;
+          View o = b.compact(md.cout, OH, OW);
+          if ((st = b.conv(cl, t, o, true, nullptr, nullptr, &x)) != HAPI_OK) return st;
+          cur = o;
+        } else {
+          // out = relu(bn(conv(t)) + idn), written in place over idn
+          if ((st = b.conv(cl, t, idn, true, &idn)) != HAPI_OK) return st;
+          cur = idn;
+        }
         i += 1;
         break;
       }
@@ -685,6 +774,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     };
     if (o.t != OP_PACK_IN) touch(o.in.buf);
     if (o.has_res) touch(o.res.buf);
+    if (o.dual) touch(o.in2.buf);
     touch(o.out.buf);
   }
   const int64_t B = m->d.max_batch;
@@ -756,12 +846,15 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.relu = o.relu;
       a.nchw = o.nchw_out;
       a.M = (long long)nb * a.OH * a.OW;
+      a.k2_chunks = o.dual ? w.K2 / 64 : 0;
+      a.stride2 = w.stride2;
       if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
         a.C = 64; a.KH = 4; a.KW = 1; a.stride = 1; a.pad = 0;
       }
       if (m->bf16) {
         ConvMaps mp;
         mp.a = (o.tc_mode >= 3) ? &o.tmap_a : nullptr;
+        mp.a2 = o.dual ? &o.tmap_a2 : nullptr;
         mp.b = &w.tmap;
         mp.y = o.nchw_out ? nullptr : &o.tmap_y;
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
@@ -842,7 +935,7 @@ hapi_status encode_view(hapi_model* m, const Plan& p, const Op& o, const View& v
   const cuuint64_t es = 2, ld = (cuuint64_t)v.ld;
   const CUtensorMapSwizzle swz = cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   void* base = vptr(m, p, v, nullptr);
-  if (o.tc_mode == 4) {
+  if (o.tc_mode == 4 || o.tc_mode == 6) {
     cuuint64_t dims[4] = {(cuuint64_t)v.C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)m->d.max_batch};
     cuuint64_t strides[3] = {ld * es, ld * es * v.W, ld * es * v.W * v.H};
     cuuint32_t box[4] = {(cuuint32_t)cols, (cuuint32_t)o.wb, (cuuint32_t)o.hb, (cuuint32_t)o.nb};
@@ -878,6 +971,16 @@ hapi_status finalize_tmaps(hapi_model* m) {
         cuuint32_t estr[4] = {1, 1, 1, 1};
         st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A");
         if (st != HAPI_OK) return st;
+      } else if (o.tc_mode == 6) {
+        void* base = vptr(m, p, o.in, nullptr);
+        const cuuint64_t ld = (cuuint64_t)o.in.ld * 2;
+        const int we = o.out.W + w.kw - 1;
+        cuuint64_t dims[4] = {(cuuint64_t)w.cs, (cuuint64_t)o.in.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+        cuuint64_t strides[3] = {ld, ld * o.in.W, ld * o.in.W * o.in.H};
+        cuuint32_t box[4] = {64, (cuuint32_t)we, (cuuint32_t)(o.hb + w.kh - 1), 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " halo");
+        if (st != HAPI_OK) return st;
       } else if (o.tc_mode == 3 || o.tc_mode == 4) {
         void* base = vptr(m, p, o.in, nullptr);
         const cuuint64_t es = 2, ld = (cuuint64_t)o.in.ld;
@@ -897,6 +1000,25 @@ hapi_status finalize_tmaps(hapi_model* m) {
         }
         if (st != HAPI_OK) return st;
       }
+      if (o.dual) {
+        void* base2 = vptr(m, p, o.in2, nullptr);
+        const cuuint64_t ld2 = (cuuint64_t)o.in2.ld * 2;
+        if (o.tc_mode == 3) {
+          cuuint64_t dims[2] = {(cuuint64_t)w.cs2, (cuuint64_t)m->d.max_batch * o.in2.H * o.in2.W};
+          cuuint64_t strides[1] = {ld2};
+          cuuint32_t box[2] = {64, 128};
+          cuuint32_t estr[2] = {1, 1};
+          st = encode_bf16(&o.tmap_a2, 2, base2, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A2");
+        } else {
+          const cuuint32_t sd = (cuuint32_t)w.stride2;
+          cuuint64_t dims[4] = {(cuuint64_t)w.cs2, (cuuint64_t)o.in2.W, (cuuint64_t)o.in2.H, (cuuint64_t)m->d.max_batch};
+          cuuint64_t strides[3] = {ld2, ld2 * o.in2.W, ld2 * o.in2.W * o.in2.H};
+          cuuint32_t box[4] = {64, (cuuint32_t)o.wb * sd, (cuuint32_t)o.hb * sd, (cuuint32_t)o.nb};
+          cuuint32_t estr[4] = {1, sd, sd, 1};
+          st = encode_bf16(&o.tmap_a2, 4, base2, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A2");
+        }
+        if (st != HAPI_OK) return st;
+      }
       if (!o.nchw_out) {
         const int cols = conv_tc_store_cols(w.bn);
         if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y")) != HAPI_OK) return st;
@@ -904,6 +1026,46 @@ hapi_status finalize_tmaps(hapi_model* m) {
       }
     }
   }
+  return HAPI_OK;
+}
+
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// One chunk through the plan, replayed from a cached CUDA graph (captured on first use;
+// PDL attributes become programmatic edges).  Falls back to direct launches if capture fails.
+hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const float* images, void* out) {
+  if (!graphs_enabled()) return run_chunk(m, p, nb, images, out, m->stream);
+  for (auto& g : m->graphs)
+    if (g.split == (uint32_t)p.split && g.nb == nb && g.images == images && g.out == out) {
+      HAPI_CUDA_TRY(cudaGraphLaunch(g.exec, m->stream));
+      return HAPI_OK;
+    }
+  if (!m->cap_stream) HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
+  HAPI_CUDA_TRY(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
+  hapi_status st = run_chunk(m, p, nb, images, out, m->cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(m->cap_stream, &graph);
+  if (st != HAPI_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return set_error(HAPI_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_error(HAPI_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(e));
+  if (m->graphs.size() >= 16) {
+    cudaGraphExecDestroy(m->graphs.front().exec);
+    m->graphs.erase(m->graphs.begin());
+  }
+  m->graphs.push_back({(uint32_t)p.split, nb, images, out, exec});
+  HAPI_CUDA_TRY(cudaGraphLaunch(exec, m->stream));
   return HAPI_OK;
 }
 
@@ -999,7 +1161,7 @@ hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* 
   const int64_t img_elems = 3ll * m->d.in_h * m->d.in_w;
   for (uint64_t c0 = 0; c0 < batch; c0 += m->d.max_batch) {
     const int nb = (int)std::min<uint64_t>(m->d.max_batch, batch - c0);
-    hapi_status st = run_chunk(m, *p, nb, images + c0 * img_elems, static_cast<char*>(out) + c0 * p->out_bytes_per_img, m->stream);
+    hapi_status st = run_chunk_graph(m, *p, nb, images + c0 * img_elems, static_cast<char*>(out) + c0 * p->out_bytes_per_img);
     if (st != HAPI_OK) return st;
   }
   return HAPI_OK;
@@ -1046,7 +1208,9 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
   }
   // ev[0..1] h2d done, ev[2..3] compute done, ev[4..5] d2h done (slot reuse)
   cudaStream_t cs = m->stream, xs = m->copy_stream;
-  const uint64_t B = m->d.max_batch;
+  // sub-chunks so the H2D copy of chunk i+1 and the D2H of chunk i-1 overlap compute of chunk i
+  uint64_t B = m->d.max_batch;
+  if (batch >= 256) B = std::min<uint64_t>(B, std::max<uint64_t>(64, (batch + 3) / 4));
   const uint64_t nchunks = (batch + B - 1) / B;
   for (uint64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c & 1);
@@ -1058,7 +1222,7 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[k], xs));
     HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[k], 0));
     if (c >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[4 + k], 0));  // stage_out[k] drained
-    hapi_status st = run_chunk(m, *p, nb, static_cast<const float*>(m->stage_in[k]), m->stage_out[k], cs);
+    hapi_status st = run_chunk_graph(m, *p, nb, static_cast<const float*>(m->stage_in[k]), m->stage_out[k]);
     if (st != HAPI_OK) return st;
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[2 + k], cs));
     HAPI_CUDA_TRY(cudaStreamWaitEvent(xs, m->ev[2 + k], 0));
@@ -1110,6 +1274,8 @@ hapi_status hapi_plan_info(const hapi_model* m, uint32_t split_idx, uint32_t* n,
 void hapi_model_destroy(hapi_model* m) {
   if (!m) return;
   cudaSetDevice(m->d.device);
+  for (auto& g : m->graphs) cudaGraphExecDestroy(g.exec);
+  if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
   if (m->host_ready) {
     cudaStreamSynchronize(m->copy_stream);
     for (auto& e : m->ev) cudaEventDestroy(e);
