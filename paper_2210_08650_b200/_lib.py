@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhapi.so")
+LIB_PATH = os.environ.get("HAPI_LIB") or os.path.join(_PKG, "libhapi.so")  # HAPI_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `python paper_2210_08650_b200/build.py` "

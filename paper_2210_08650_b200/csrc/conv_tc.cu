@@ -64,7 +64,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 512 /*barriers*/;
-  static_assert((2 * MAX_B_STAGES + 2 * MAX_A_STAGES + 8) * 8 + 4 <= 512, "barrier area");
+  static_assert((2 * MAX_B_STAGES + 2 * MAX_A_STAGES + 9) * 8 + 4 <= 512, "barrier area");
   static int stages(bool res) {
     int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
     return s > MAX_STAGES ? MAX_STAGES : s;
@@ -222,6 +222,8 @@ struct Geo {
   int has_res;                 // residual tiles streamed by the loader warp
   int tma_out;                 // 1: epilogue writes via TMA store (NHWC views); 0: NCHW direct
   int res_box_bytes;           // bytes of one residual box
+  int b_res;                   // 1: all weight chunks resident in smem (one N tile), loaded once
+  int cps;                     // K chunks per pipeline stage (modes 3/4: 2 when BN <= 128)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -283,12 +285,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool SPATIAL = (MODE == 4 || MODE == 6);
   const int S = g.stages;
   const int AS = MODE == 6 ? g.a_stages : S;
-  const int ASZ = MODE == 6 ? g.a_stage_bytes : A_STAGE_BYTES;
+  constexpr int CPS = (MODE == 3 && BN <= 128) ? 2 : 1;  // == g.cps (host); mode 4 measured better at 1
+  const int ASZ = MODE == 6 ? g.a_stage_bytes : CPS * A_STAGE_BYTES;   // A ring slot
+  const int BSZ = CPS * C::B_STAGE_BYTES;                               // B ring slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + AS * ASZ;
-  uint8_t* sY = sB + S * C::B_STAGE_BYTES;                 // 2 output staging blocks
+  uint8_t* sY = sB + (g.b_res ? g.k_chunks * C::B_STAGE_BYTES : S * BSZ);  // 2 output staging blocks
   uint8_t* sR = sY + 2 * C::SB_BYTES;                      // 2 residual blocks (if has_res)
   float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? 2 * C::SB_BYTES : 0));
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias + BN);
@@ -299,7 +303,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
   uint64_t* rempty = rfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + 2);
+  uint64_t* bres = rempty + 2;               // resident weights landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&rfull[i], 1);
       mbar_init(&rempty[i], NUM_EPI_THREADS);
     }
+    mbar_init(bres, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == PROD_WARP0 && lane == 0) {
@@ -344,6 +350,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ producer
     const int pt = threadIdx.x - PROD_WARP0 * 32;
+    if (TMA_A && g.b_res && warp == PROD_WARP0) {
+      // all weight chunks of the single N tile, once per CTA
+      if (elect_one()) {
+        mbar_arrive_expect_tx(bres, (uint32_t)g.k_chunks * C::B_STAGE_BYTES);
+        for (int c = 0; c < g.k_chunks; ++c)
+          tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b, c * BK, 0, bres);
+      }
+      __syncwarp();
+    }
     if (MODE == 6) {
       // halo mode: one [(hb+KH-1) x we] pixel box per 64-channel block, then the taps' weights
       if (warp == PROD_WARP0) {
@@ -361,6 +376,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             __syncwarp();
             if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
+            if (g.b_res) continue;
             for (int t = 0; t < taps; ++t) {
               mbar_wait(&empty[stage], phase ^ 1);
               if (elect_one()) {
@@ -385,30 +401,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             h0 = oh0 * a.stride - a.pad;
           }
           int cb = 0, r = 0, sft = 0;  // (tap, channel block) of chunk kc, tracked incrementally
-          for (int kc = 0; kc < g.k_chunks; ++kc) {
+          for (int kc = 0; kc < g.k_chunks; kc += CPS) {
+            const int nch = g.k_chunks - kc < CPS ? g.k_chunks - kc : CPS;
             mbar_wait(&empty[stage], phase ^ 1);
             if (elect_one()) {
-              const uint32_t dA = smem_u32(sA + stage * A_STAGE_BYTES);
-              mbar_arrive_expect_tx(&full[stage], g.a_bytes + C::B_STAGE_BYTES);
-              if (kc >= g.k1_chunks) {
-                // fused downsample: 1x1 conv with stride2 over the block input
-                const int c2 = kc - g.k1_chunks;
-                if (MODE == 3)
-                  tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
-                else
-                  tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
-              } else if (MODE == 3) {
-                tma_load_2d(dA, &tmap_a, kc * BK, tm * BM, &full[stage]);
-              } else {
-                tma_load_4d(dA, &tmap_a, cb * BK, w0 + sft, h0 + r, b0, &full[stage]);
+              mbar_arrive_expect_tx(&full[stage], nch * (g.a_bytes + (g.b_res ? 0 : C::B_STAGE_BYTES)));
+              int cb_j = cb, r_j = r, s_j = sft;
+              for (int j = 0; j < nch; ++j) {
+                const int ck = kc + j;
+                const uint32_t dA = smem_u32(sA + stage * ASZ + j * A_STAGE_BYTES);
+                if (ck >= g.k1_chunks) {
+                  // fused downsample: 1x1 conv with stride2 over the block input
+                  const int c2 = ck - g.k1_chunks;
+                  if (MODE == 3)
+                    tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
+                  else
+                    tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
+                } else if (MODE == 3) {
+                  tma_load_2d(dA, &tmap_a, ck * BK, tm * BM, &full[stage]);
+                } else {
+                  tma_load_4d(dA, &tmap_a, cb_j * BK, w0 + s_j, h0 + r_j, b0, &full[stage]);
+                }
+                if (!g.b_res)
+                  tma_load_2d(smem_u32(sB + stage * BSZ + j * C::B_STAGE_BYTES), &tmap_b, ck * BK, tn * BN, &full[stage]);
+                if (++cb_j == g.cblocks) {
+                  cb_j = 0;
+                  if (++s_j == a.KW) { s_j = 0; ++r_j; }
+                }
               }
-              tma_load_2d(smem_u32(sB + stage * C::B_STAGE_BYTES), &tmap_b, kc * BK, tn * BN, &full[stage]);
             }
             __syncwarp();
             if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
-            if (++cb == g.cblocks) {
-              cb = 0;
-              if (++sft == a.KW) { sft = 0; ++r; }
+            for (int j = 0; j < nch; ++j) {
+              if (++cb == g.cblocks) {
+                cb = 0;
+                if (++sft == a.KW) { sft = 0; ++r; }
+              }
             }
           }
         }
@@ -520,6 +548,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                              ((uint32_t)(BM >> 4) << 24);
       const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
       uint32_t stage = 0, phase = 0, ast = 0, aph = 0;
+      if (TMA_A && g.b_res) mbar_wait(bres, 0);
       int iter = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
         const int acc = iter & 1;
@@ -536,20 +565,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             mbar_wait(&afull[ast], aph);
             tc_fence_after();
             const uint32_t a_base = sA0 + ast * ASZ;
+            if (g.b_res) {
+              // weights resident: all taps of this channel block in one burst
+              if (elect_one()) {
+                int r = 0, sft = 0;
+                for (int t = 0; t < taps; ++t) {
+                  const uint64_t adesc = make_sdesc_rows(a_base, r * g.we + sft);
+                  const uint64_t bdesc = make_sdesc(sB0 + (t * g.cblocks + cb) * C::B_STAGE_BYTES);
+#pragma unroll
+                  for (int k = 0; k < BK / 16; ++k)
+                    mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cb | t | k) != 0);
+                  if (++sft == a.KW) { sft = 0; ++r; }
+                }
+                mma_commit(&aempty[ast]);
+              }
+              __syncwarp();
+              if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
+              continue;
+            }
             int r = 0, sft = 0;
             for (int t = 0; t < taps; ++t) {
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
+              if (!g.b_res) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+              }
               const uint64_t adesc = make_sdesc_rows(a_base, r * g.we + sft);
-              const uint64_t bdesc = make_sdesc(sB0 + stage * C::B_STAGE_BYTES);
+              const uint64_t bdesc = make_sdesc(sB0 + (g.b_res ? (t * g.cblocks + cb) : (int)stage) * C::B_STAGE_BYTES);
               if (elect_one()) {
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k) mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum | k);
-                mma_commit(&empty[stage]);
+                if (!g.b_res) mma_commit(&empty[stage]);
               }
               __syncwarp();
               accum = 1;
-              if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+              if (!g.b_res && ++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
               if (++sft == a.KW) { sft = 0; ++r; }
             }
             if (elect_one()) mma_commit(&aempty[ast]);
@@ -560,19 +609,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           continue;
         }
-        for (int kc = 0; kc < g.k_chunks; ++kc) {
+        for (int kc = 0; kc < g.k_chunks; kc += CPS) {
+          const int nch = g.k_chunks - kc < CPS ? g.k_chunks - kc : CPS;
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint64_t adesc = make_sdesc(sA0 + stage * A_STAGE_BYTES);
-          const uint64_t bdesc = make_sdesc(sB0 + stage * C::B_STAGE_BYTES);
           if (elect_one()) {
+            for (int j = 0; j < nch; ++j) {
+              const uint64_t adesc = make_sdesc(sA0 + stage * ASZ + j * A_STAGE_BYTES);
+              const uint64_t bdesc =
+                  make_sdesc(g.b_res ? sB0 + (kc + j) * C::B_STAGE_BYTES : sB0 + stage * BSZ + j * C::B_STAGE_BYTES);
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k) {
-              // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle atom
-              mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kc | k) != 0);
+              for (int k = 0; k < BK / 16; ++k) {
+                // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle atom
+                mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kc + j) | k) != 0);
+              }
             }
             mma_commit(&empty[stage]);
-            if (kc == g.k_chunks - 1) mma_commit(&tfull[acc]);
+            if (kc + nch >= g.k_chunks) mma_commit(&tfull[acc]);
           }
           __syncwarp();
           if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
@@ -741,6 +794,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+bool bres_enabled() {  // HAPI_BRES=1: also keep weights resident in modes 3/4 (experiment)
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_BRES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int BN, int MODE>
 cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, cudaStream_t st) {
   using C = Cfg<BN>;
@@ -753,16 +814,35 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   }
   g.res_box_bytes = (g.mode == 4 || g.mode == 6) ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
   int smem;
+  const int res_bytes = g.has_res ? 2 * C::SB_BYTES : 0;
+  const int bres_bytes = g.k_chunks * C::B_STAGE_BYTES;
+  const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 6;
+  const int a_min = g.mode == 6 ? g.a_stages * g.a_stage_bytes : 4 * A_STAGE_BYTES;
+  // resident weights: measured win in halo mode; in modes 3/4 (e.g. the stem) it was slower
+  g.b_res = tma_a && g.n_tiles == 1 && (g.mode == 6 || bres_enabled()) &&
+            C::FIXED + res_bytes + a_min + bres_bytes <= SMEM_LIMIT;
+  g.cps = (g.mode == 3 && BN <= 128) ? 2 : 1;
   if (g.mode == 6) {
-    const int rest = SMEM_LIMIT - C::FIXED - (g.has_res ? 2 * C::SB_BYTES : 0) - g.a_stages * g.a_stage_bytes;
-    g.stages = rest / C::B_STAGE_BYTES;
-    if (g.stages > MAX_B_STAGES) g.stages = MAX_B_STAGES;
-    if (g.stages < 2) return cudaErrorInvalidValue;
-    smem = g.a_stages * g.a_stage_bytes + g.stages * C::B_STAGE_BYTES + C::FIXED + (g.has_res ? 2 * C::SB_BYTES : 0);
+    if (g.b_res) {
+      g.stages = 1;  // B ring unused
+      smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED + res_bytes;
+    } else {
+      const int rest = SMEM_LIMIT - C::FIXED - res_bytes - g.a_stages * g.a_stage_bytes;
+      g.stages = rest / C::B_STAGE_BYTES;
+      if (g.stages > MAX_B_STAGES) g.stages = MAX_B_STAGES;
+      if (g.stages < 2) return cudaErrorInvalidValue;
+      smem = g.a_stages * g.a_stage_bytes + g.stages * C::B_STAGE_BYTES + C::FIXED + res_bytes;
+    }
+  } else if (g.b_res) {
+    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - bres_bytes) / (g.cps * A_STAGE_BYTES);
+    if (g.stages > MAX_STAGES) g.stages = MAX_STAGES;
+    smem = g.stages * g.cps * A_STAGE_BYTES + bres_bytes + C::FIXED + res_bytes;
   } else {
-    g.stages = C::stages(g.has_res);
-    smem = C::smem_bytes(g.stages, g.has_res);
+    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes) / (g.cps * C::STAGE_BYTES);
+    if (g.stages > MAX_STAGES) g.stages = MAX_STAGES;
+    smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes;
   }
+  if (g.stages < 2 && !(g.mode == 6 && g.b_res)) return cudaErrorInvalidValue;
   const int tiles = g.m_tiles * g.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
   if (grid <= 0) return cudaSuccess;

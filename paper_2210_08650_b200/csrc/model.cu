@@ -898,7 +898,8 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       e = pack_output_launch(vptr(m, p, o.in, out), nb, o.in.H * o.in.W, o.in.C, o.in.ld, out, isb, st);
       break;
   }
-  if (e != cudaSuccess) return set_error(HAPI_ERR_CUDA, "launch of op %d failed: %s", (int)o.t, cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    return set_error(HAPI_ERR_CUDA, "launch of %s failed: %s", o.desc.empty() ? "op" : o.desc.c_str(), cudaGetErrorString(e));
   return HAPI_OK;
 }
 
