@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (arch, act, split, batch per GPU, image seed)
+    # name: (arch, act, split, batch per GPU, image seed)            -- weak scaling
     "resnet50_s21_b512": ("resnet50", "bf16", 21, 512, 3),
     "resnet50_s20_b512": ("resnet50", "bf16", 20, 512, 3),
     "resnet18_s10_b200": ("resnet18", "bf16", 10, 200, 2),
@@ -34,6 +34,14 @@ WORKLOADS = {
     "densenet121_s20_b512": ("densenet121", "bf16", 20, 512, 5),
     "vgg11_s21_b256": ("vgg11", "bf16", 21, 256, 4),
 }
+# configs[4]: 65,536 images sharded over the ranks (strong scaling), COS batch 512;
+# name: (arch, act, split, total images, seed)
+STRONG = {
+    "resnet50_s21_64k": ("resnet50", "bf16", 21, 65536, 5),
+    "densenet121_s9_64k": ("densenet121", "bf16", 9, 65536, 5),
+    "densenet121_s20_64k": ("densenet121", "bf16", 20, 65536, 5),
+}
+STRONG_COS_BATCH = 512
 METRIC = "prefix-forward images/sec at split layer"
 L2_BYTES = 126 * 1024 * 1024
 
@@ -60,7 +68,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:  # noqa: BLE001
             self.proc = None
@@ -155,6 +163,12 @@ def run_reference(args, wl):
 
 
 def config_of(wl, n):
+    if wl in STRONG:
+        arch, act, split, total, _ = STRONG[wl]
+        return {"workload": wl, "split_idx": split, "total_images": total, "cos_batch": STRONG_COS_BATCH,
+                "image": "3x224x224 fp32 NCHW, N(0,1) (generated on device, seeded per rank)",
+                "weights": "random-init (seeded), BN folded", "l2": "inputs larger than L2",
+                "parallelism": f"dp{n} (contiguous shards of the {total} images, no data-path collective)"}
     arch, act, split, batch, _ = WORKLOADS[wl]
     return {"workload": wl, "split_idx": split, "batch_per_gpu": batch, "global_batch": batch * n,
             "image": "3x224x224 fp32 NCHW, N(0,1)", "weights": "random-init (seeded), BN folded",
@@ -163,12 +177,73 @@ def config_of(wl, n):
             "parallelism": f"dp{n} (contiguous image shards, no data-path collective)"}
 
 
+def run_strong(args, wl):
+    """configs[4]: a fixed set of images sharded over the ranks; one step = every rank runs
+    its whole shard (chunked at the COS batch inside hapi_prefix_forward)."""
+    import torch
+    import torch.distributed as dist
+
+    import hapi_inputs
+    import paper_2210_08650_b200 as H
+    from paper_2210_08650_b200.parallel import gather_meta, shard_range, summarize
+
+    arch, act, split, total, seed = STRONG[wl]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    a, b = shard_range(total, world, rank)
+    n = b - a
+    model = H.Model(arch, act, list(hapi_inputs.params(arch, 1000 + seed).values()), STRONG_COS_BATCH, split, split,
+                    device=local)
+    stream = torch.cuda.current_stream()
+    model.set_stream(stream.cuda_stream)
+    gen = torch.Generator(device="cuda").manual_seed(seed * 1000 + rank)
+    x = torch.randn(n, 3, 224, 224, generator=gen, device="cuda")
+    out = torch.empty(model.out_bytes[split - 1] // 2 * n, dtype=torch.bfloat16, device="cuda")
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(max(1, args.warmup // 3)):
+        model.forward(split, x, out)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    steps = max(1, args.steps // 10)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            model.forward(split, x, out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    meta = gather_meta(n * steps, int(ms * 1e6), float(out.float().sum().item()), device="cuda")
+    tot, tmax, rate, checks = summarize(meta)
+    if rank == 0:
+        info = model.plan_info(split)
+        print(json.dumps({
+            "metric": METRIC, "value": rate, "unit": "img/s", "n_gpus": world, "steps": steps,
+            "warmup": max(1, args.warmup // 3), "ms_per_step": tmax * 1e3 / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": act, "data": "synthetic", "config": config_of(wl, world),
+            "clocks": clk.summary(), "e2e": None, "gpu_launches": int(info["n"]) * ((total // world + 511) // 512) * steps,
+            "checksum_ranks": checks}), flush=True)
+    model.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="resnet50_s21_b512", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="resnet50_s21_b512", choices=sorted(WORKLOADS) + sorted(STRONG))
     ap.add_argument("--impl", default="hapi", choices=["hapi", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -177,6 +252,8 @@ def main():
     wl = args.workload
     if args.impl == "reference":
         return run_reference(args, wl)
+    if wl in STRONG:
+        return run_strong(args, wl)
 
     import numpy as np
     import torch
@@ -241,17 +318,10 @@ def main():
     torch.cuda.synchronize()
     checksum = float(out.float().sum().item())
     # max over ranks (NCCL all_gather of [count, elapsed_ns, checksum bits])
-    meta = torch.tensor([batch * args.steps, int(ms * 1e6), int(np.float64(checksum).view(np.int64))],
-                        dtype=torch.int64, device="cuda")
-    if world > 1:
-        allm = torch.empty(world * 3, dtype=torch.int64, device="cuda")
-        dist.all_gather_into_tensor(allm, meta)
-        allm = allm.view(world, 3).cpu().numpy()
-    else:
-        allm = meta.view(1, 3).cpu().numpy()
-    max_ms = allm[:, 1].max() / 1e6
-    total_imgs = int(allm[:, 0].sum())
-    value = total_imgs / (max_ms / 1e3)
+    from paper_2210_08650_b200.parallel import gather_meta, summarize
+    allm = gather_meta(batch * args.steps, int(ms * 1e6), checksum, device="cuda")
+    total_imgs, max_s, value, checks = summarize(allm)
+    max_ms = max_s * 1e3
 
     # per-launch profile (separate pass with CUDA events between launches)
     info = model.plan_info(split)
@@ -333,7 +403,7 @@ def main():
             "roofline": roof, "kernel_class_share": class_share, "cpu_baseline": cpu, "clocks": clk.summary(),
             "e2e": e2e, "gpu_launches": int(info["n"] - sum(1 for k in info["kind"] if k == 3 and False)) * args.steps,
             "gpu_launches_per_step": int(info["n"]),
-            "checksum_ranks": [float(np.int64(v).view(np.float64)) for v in allm[:, 2]],
+            "checksum_ranks": checks,
         }
         print(json.dumps(line), flush=True)
     model.close()

@@ -1160,9 +1160,14 @@ hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* 
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
   HAPI_CUDA_TRY(cudaGetLastError());
   const int64_t img_elems = 3ll * m->d.in_h * m->d.in_w;
+  // graphs are keyed by the chunk's pointers: replay them for calls of up to a few chunks,
+  // launch directly when a large call would only thrash the cache
+  const bool use_graph = (batch + m->d.max_batch - 1) / m->d.max_batch <= 4;
   for (uint64_t c0 = 0; c0 < batch; c0 += m->d.max_batch) {
     const int nb = (int)std::min<uint64_t>(m->d.max_batch, batch - c0);
-    hapi_status st = run_chunk_graph(m, *p, nb, images + c0 * img_elems, static_cast<char*>(out) + c0 * p->out_bytes_per_img);
+    const float* ci = images + c0 * img_elems;
+    void* co = static_cast<char*>(out) + c0 * p->out_bytes_per_img;
+    hapi_status st = use_graph ? run_chunk_graph(m, *p, nb, ci, co) : run_chunk(m, *p, nb, ci, co, m->stream);
     if (st != HAPI_OK) return st;
   }
   return HAPI_OK;
