@@ -46,7 +46,8 @@ constexpr int PROD_WARP0 = 8;
 constexpr int NUM_PROD_THREADS = 128;
 constexpr int MMA_WARP = 12;
 constexpr int RES_WARP = 13;
-constexpr int NUM_THREADS = 14 * 32;
+constexpr int XFORM_TMA_WARP = 14;   // mode 7: TMA issuer while warps 8-11 transform
+constexpr int NUM_THREADS = 15 * 32;
 constexpr int A_STAGE_BYTES = BM * BK * 2;
 constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in per CTA
 constexpr int MAX_STAGES = 8;
@@ -63,8 +64,8 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 512 /*barriers*/;
-  static_assert((2 * MAX_B_STAGES + 2 * MAX_A_STAGES + 9) * 8 + 4 <= 512, "barrier area");
+  static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 1024 /*barriers*/;
+  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 9) * 8 + 4 <= 1024, "barrier area");
   static int stages(bool res) {
     int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
     return s > MAX_STAGES ? MAX_STAGES : s;
@@ -90,9 +91,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0;
   uint32_t spins = 0;
+  uint64_t t0 = 0;
   while (!done) {
-    // watchdog: a lost arrival must fail loudly instead of hanging the GPU
-    if (++spins == (1u << 30)) __trap();
+    // watchdog: a lost arrival must fail loudly (trap after ~2 s) instead of hanging the GPU
+    if ((++spins & 1023u) == 0) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 2000000000ull) __trap();
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -224,6 +231,7 @@ struct Geo {
   int res_box_bytes;           // bytes of one residual box
   int b_res;                   // 1: all weight chunks resident in smem (one N tile), loaded once
   int cps;                     // K chunks per pipeline stage (modes 3/4: 2 when BN <= 128)
+  int pro_c;                   // mode 7: channels of the smem scale/shift tables (C rounded to 64)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 6);
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 6 || MODE == 7);
   constexpr bool SPATIAL = (MODE == 4 || MODE == 6);
   const int S = g.stages;
   const int AS = MODE == 6 ? g.a_stages : S;
@@ -295,7 +303,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sY = sB + (g.b_res ? g.k_chunks * C::B_STAGE_BYTES : S * BSZ);  // 2 output staging blocks
   uint8_t* sR = sY + 2 * C::SB_BYTES;                      // 2 residual blocks (if has_res)
   float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? 2 * C::SB_BYTES : 0));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sBias + BN);
+  float* sScale = sBias + BN;                                   // mode 7 prologue tables
+  float* sShift = sScale + (MODE == 7 ? g.pro_c : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sShift + (MODE == 7 ? g.pro_c : 0));
   uint64_t* empty = full + MAX_B_STAGES;
   uint64_t* afull = empty + MAX_B_STAGES;    // mode 6 halo ring
   uint64_t* aempty = afull + MAX_A_STAGES;
@@ -304,7 +314,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* rfull = tempty + 2;
   uint64_t* rempty = rfull + 2;
   uint64_t* bres = rempty + 2;               // resident weights landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+  uint64_t* lfull = bres + 1;                // mode 7: raw A tile landed (before the transform)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + MAX_B_STAGES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -312,8 +323,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], TMA_A ? 1 : NUM_PROD_THREADS + 1);
+      mbar_init(&full[s], MODE == 7 ? NUM_PROD_THREADS : (TMA_A ? 1 : NUM_PROD_THREADS + 1));
       mbar_init(&empty[s], 1);
+      mbar_init(&lfull[s], 1);
     }
     for (int i = 0; i < MAX_A_STAGES; ++i) {
       mbar_init(&afull[i], 1);
@@ -347,7 +359,75 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_tiles = g.m_tiles * g.n_tiles;
   const int OHW = a.OH * a.OW;
 
-  if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
+  if (MODE == 7 && warp == XFORM_TMA_WARP) {
+    // ================================================================ mode 7 loader
+    uint32_t stage = 0, phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+      for (int kc = 0; kc < g.k_chunks; ++kc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          mbar_arrive_expect_tx(&lfull[stage], g.a_bytes + C::B_STAGE_BYTES);
+          tma_load_2d(smem_u32(sA + stage * ASZ), &tmap_a, kc * BK, tm * BM, &lfull[stage]);
+          tma_load_2d(smem_u32(sB + stage * BSZ), &tmap_b, kc * BK, tn * BN, &lfull[stage]);
+        }
+        __syncwarp();
+        if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (MODE == 7 && warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
+    // ================================================================ mode 7 transform
+    // bn-relu prologue applied in shared memory: thread = tile row, its 8 swizzled 16-byte
+    // chunks (conflict-free), channel = chunk ^ (row & 7) inside the 64-channel block
+    const int pt = threadIdx.x - PROD_WARP0 * 32;
+    for (int i = pt; i < g.pro_c; i += NUM_PROD_THREADS) {
+      sScale[i] = i < a.C ? __ldg(a.pro_scale + i) : 0.f;
+      sShift[i] = i < a.C ? __ldg(a.pro_shift + i) : 0.f;
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    // thread -> logical 8-channel group j = pt % 8 of rows pt/8 + 16 i: the group's scale and
+    // shift live in registers for the whole stage; 8 consecutive threads cover one 128-byte
+    // row (conflict-free), physical chunk = j ^ (row & 7)
+    const int j = pt & 7, r0 = pt >> 3;
+    uint32_t stage = 0, phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int kc = 0; kc < g.k_chunks; ++kc) {
+        const int c0 = kc * BK + j * 8;
+        const float4 s0 = *reinterpret_cast<const float4*>(sScale + c0);
+        const float4 s1 = *reinterpret_cast<const float4*>(sScale + c0 + 4);
+        const float4 h0 = *reinterpret_cast<const float4*>(sShift + c0);
+        const float4 h1 = *reinterpret_cast<const float4*>(sShift + c0 + 4);
+        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+        const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+        mbar_wait(&lfull[stage], phase);
+        const uint32_t base = smem_u32(sA + stage * ASZ);
+        uint32_t w[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 16 * i;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[i][0]), "=r"(w[i][1]), "=r"(w[i][2]), "=r"(w[i][3])
+                       : "r"(base + r * 128 + ((j ^ (r & 7)) << 4)));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = r0 + 16 * i;
+          uint32_t o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = unpack_bf16x2(w[i][q]);
+            o[q] = pack_bf16x2(fmaxf(fmaf(f.x, sc[2 * q], sh[2 * q]), 0.f), fmaxf(fmaf(f.y, sc[2 * q + 1], sh[2 * q + 1]), 0.f));
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + r * 128 + ((j ^ (r & 7)) << 4)),
+                       "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&full[stage]);
+        if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ producer
     const int pt = threadIdx.x - PROD_WARP0 * 32;
     if (TMA_A && g.b_res && warp == PROD_WARP0) {
@@ -657,7 +737,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else {
+  } else if (warp < NUM_EPI_WARPS) {
     // ================================================================ epilogue
     // Thread = tile row (its TMEM lane); warps w and w+4 share lane quarter w%4 and take
     // alternate 32-column sub-chunks.  Per SB-column block: TMEM -> registers, + bias
@@ -822,6 +902,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   g.b_res = tma_a && g.n_tiles == 1 && (g.mode == 6 || bres_enabled()) &&
             C::FIXED + res_bytes + a_min + bres_bytes <= SMEM_LIMIT;
   g.cps = (g.mode == 3 && BN <= 128) ? 2 : 1;
+  const int pro_bytes = g.mode == 7 ? 8 * g.pro_c : 0;
   if (g.mode == 6) {
     if (g.b_res) {
       g.stages = 1;  // B ring unused
@@ -838,9 +919,9 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
     if (g.stages > MAX_STAGES) g.stages = MAX_STAGES;
     smem = g.stages * g.cps * A_STAGE_BYTES + bres_bytes + C::FIXED + res_bytes;
   } else {
-    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes) / (g.cps * C::STAGE_BYTES);
+    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - pro_bytes) / (g.cps * C::STAGE_BYTES);
     if (g.stages > MAX_STAGES) g.stages = MAX_STAGES;
-    smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes;
+    smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes + pro_bytes;
   }
   if (g.stages < 2 && !(g.mode == 6 && g.b_res)) return cudaErrorInvalidValue;
   const int tiles = g.m_tiles * g.n_tiles;
@@ -859,6 +940,7 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
     case 6: return launch_t<BN, 6>(a, g, mp, num_sms, st);
+    case 7: return launch_t<BN, 7>(a, g, mp, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -924,6 +1006,12 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     g.k_chunks = (a.K + BK - 1) / BK;
     g.cblocks = a.C / BK;
     g.a_bytes = A_STAGE_BYTES;
+    if (mode == 7) {
+      // TMA-loaded 1x1 A with the bn-relu prologue applied in smem (C % 8 == 0)
+      if (a.KH != 1 || a.KW != 1 || a.stride != 1 || a.pad != 0 || a.C % 8 != 0 || !a.pro_scale || !mp.a)
+        return cudaErrorInvalidValue;
+      g.pro_c = (a.C + BK - 1) / BK * BK;
+    }
   }
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {

@@ -62,6 +62,14 @@ EncodeTiledFn get_encode_fn() {
   return fn;
 }
 
+bool prologue_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_PRO_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool halo_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_HALO");
@@ -414,7 +422,9 @@ struct Builder {
     const ConvW& w = m->convs[ci];
     if (m->bf16) {
       o.tc_mode = w.mode;
-      if (in2) {
+      if (w.mode == 2 && w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0 && prologue_tma_enabled()) {
+        o.tc_mode = 7;  // TMA-loaded A, bn-relu applied in shared memory
+      } else if (in2) {
         // fused downsample: both A sources must produce rows in the same order
         if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0 && cs.stride2 == 1) {
           o.tc_mode = 3;
@@ -982,10 +992,10 @@ hapi_status finalize_tmaps(hapi_model* m) {
         cuuint32_t estr[4] = {1, 1, 1, 1};
         st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " halo");
         if (st != HAPI_OK) return st;
-      } else if (o.tc_mode == 3 || o.tc_mode == 4) {
+      } else if (o.tc_mode == 3 || o.tc_mode == 4 || o.tc_mode == 7) {
         void* base = vptr(m, p, o.in, nullptr);
         const cuuint64_t es = 2, ld = (cuuint64_t)o.in.ld;
-        if (o.tc_mode == 3) {
+        if (o.tc_mode == 3 || o.tc_mode == 7) {
           cuuint64_t dims[2] = {(cuuint64_t)w.cs, (cuuint64_t)m->d.max_batch * o.in.H * o.in.W};
           cuuint64_t strides[1] = {ld * es};
           cuuint32_t box[2] = {64, 128};
