@@ -52,7 +52,7 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;
 constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in per CTA
 constexpr int MAX_STAGES = 8;
 constexpr int MAX_B_STAGES = 16;  // mode 6 weight ring
-constexpr int MAX_A_STAGES = 2;   // mode 6 halo ring
+constexpr int MAX_A_STAGES = 8;   // mode 6 / mode 8 halo rings
 
 // Static part of the shared-memory carve-up; the pipeline depth is chosen per launch.
 template <int BN>
@@ -126,6 +126,11 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_load_1d(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                             uint64_t* bar) {
   asm volatile(
@@ -180,6 +185,18 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr) {
 __device__ __forceinline__ uint64_t make_sdesc_rows(uint32_t base, int row_off) {
   return make_sdesc(base + (uint32_t)row_off * 128u);
 }
+// SMEM matrix descriptor, K-major, no swizzle: core matrices of 8 rows x 16 B (128 B
+// contiguous); `lbo` = byte distance between the two K-adjacent core matrices of a K=16
+// step, `sbo` = byte distance between 8-row groups.  Any 16-byte-aligned start works, so a
+// row shift is a plain address offset (mode 8 taps).
+__device__ __forceinline__ uint64_t make_sdesc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -232,6 +249,7 @@ struct Geo {
   int b_res;                   // 1: all weight chunks resident in smem (one N tile), loaded once
   int cps;                     // K chunks per pipeline stage (modes 3/4: 2 when BN <= 128)
   int pro_c;                   // mode 7: channels of the smem scale/shift tables (C rounded to 64)
+  int ph, pw, pq, strips, n_tasks;  // mode 8: pooled map, pool columns per strip, strips/image, tasks
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -259,8 +277,26 @@ __device__ __forceinline__ long long row_to_m(const ConvArgs& a, const Geo& g, i
   return ((long long)n * a.OH + oh) * a.OW + ow;
 }
 
+// k-th tile of this CTA (-1 when done).  Mode 8 hands out whole (image, strip) tasks so a
+// CTA walks one strip's pooled rows in order (the previous stem row stays in smem).
+__device__ __forceinline__ int tile_at(const Geo& g, int k, int num_tiles) {
+  if (g.mode == 8) {
+    const int task = blockIdx.x + (k / g.ph) * gridDim.x;
+    return task < g.n_tasks ? task * g.ph + (k - (k / g.ph) * g.ph) : -1;
+  }
+  const int t = blockIdx.x + k * gridDim.x;
+  return t < num_tiles ? t : -1;
+}
+
 // Spatial origin of m-tile tm in mode 4 (output coordinates).
 __device__ __forceinline__ void tile_origin(const Geo& g, int tm, int* w0, int* h0, int* b0) {
+  if (g.mode == 8) {  // stem rows 2po, 2po+1, stem columns from 2 q0 - 1 (pool padding)
+    const int po = tm % g.ph, task = tm / g.ph;
+    *b0 = task / g.strips;
+    *w0 = 2 * (task % g.strips) * g.pq - 1;
+    *h0 = 2 * po;
+    return;
+  }
   const int tw = tm % g.tiles_w, th = (tm / g.tiles_w) % g.tiles_h, tb = tm / (g.tiles_w * g.tiles_h);
   *w0 = tw * g.wb;
   *h0 = th * g.hb;
@@ -289,12 +325,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 6 || MODE == 7);
-  constexpr bool SPATIAL = (MODE == 4 || MODE == 6);
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8);
+  constexpr bool SPATIAL = (MODE == 4 || MODE == 6 || MODE == 8);
   const int S = g.stages;
-  const int AS = MODE == 6 ? g.a_stages : S;
+  const int AS = (MODE == 6 || MODE == 8) ? g.a_stages : S;
   constexpr int CPS = (MODE == 3 && BN <= 128) ? 2 : 1;  // == g.cps (host); mode 4 measured better at 1
-  const int ASZ = MODE == 6 ? g.a_stage_bytes : CPS * A_STAGE_BYTES;   // A ring slot
+  const int ASZ = (MODE == 6 || MODE == 8) ? g.a_stage_bytes : CPS * A_STAGE_BYTES;   // A ring slot
   const int BSZ = CPS * C::B_STAGE_BYTES;                               // B ring slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -362,7 +398,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (MODE == 7 && warp == XFORM_TMA_WARP) {
     // ================================================================ mode 7 loader
     uint32_t stage = 0, phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
       const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
       for (int kc = 0; kc < g.k_chunks; ++kc) {
         mbar_wait(&empty[stage], phase ^ 1);
@@ -390,7 +426,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // row (conflict-free), physical chunk = j ^ (row & 7)
     const int j = pt & 7, r0 = pt >> 3;
     uint32_t stage = 0, phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
       for (int kc = 0; kc < g.k_chunks; ++kc) {
         const int c0 = kc * BK + j * 8;
         const float4 s0 = *reinterpret_cast<const float4*>(sScale + c0);
@@ -430,7 +466,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ producer
     const int pt = threadIdx.x - PROD_WARP0 * 32;
-    if (TMA_A && g.b_res && warp == PROD_WARP0) {
+    if (TMA_A && MODE != 8 && g.b_res && warp == PROD_WARP0) {
       // all weight chunks of the single N tile, once per CTA
       if (elect_one()) {
         mbar_arrive_expect_tx(bres, (uint32_t)g.k_chunks * C::B_STAGE_BYTES);
@@ -439,12 +475,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       __syncwarp();
     }
-    if (MODE == 6) {
+    if (MODE == 8) {
+      // stem halo: resident weights once, then per tile one [5 rows x we] box of the padded
+      // s2d input as two 16-byte-per-pixel planes (channels 0-7 | 8-15)
+      if (warp == PROD_WARP0) {
+        if (elect_one()) {
+          mbar_arrive_expect_tx(bres, 16 * 2 * 64 * 16);
+          bulk_load_1d(smem_u32(sB), a.w, 16 * 2 * 64 * 16, bres);
+        }
+        __syncwarp();
+        uint32_t ast = 0, aph = 0;
+        const uint32_t plane = (uint32_t)g.a_bytes / 2;
+        const uint32_t plane_stride = (plane + 127) / 128 * 128;
+        for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
+          int w0, h0, b0;
+          tile_origin(g, tile, &w0, &h0, &b0);
+          mbar_wait(&aempty[ast], aph ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&afull[ast], g.a_bytes);
+            const uint32_t dst = smem_u32(sA + ast * ASZ);
+            tma_load_4d(dst, &tmap_a, 0, w0, h0, b0, &afull[ast]);
+            tma_load_4d(dst + plane_stride, &tmap_a, 8, w0, h0, b0, &afull[ast]);
+          }
+          __syncwarp();
+          if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
+        }
+      }
+    } else if (MODE == 6) {
       // halo mode: one [(hb+KH-1) x we] pixel box per 64-channel block, then the taps' weights
       if (warp == PROD_WARP0) {
         uint32_t stage = 0, phase = 0, ast = 0, aph = 0;
         const int taps = a.KH * a.KW;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
           const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
           int ow0, oh0, b0;
           tile_origin(g, tm, &ow0, &oh0, &b0);
@@ -472,7 +534,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     } else if (TMA_A) {
       if (warp == PROD_WARP0) {
         uint32_t stage = 0, phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
           const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
           int ow0 = 0, oh0 = 0, b0 = 0, w0 = 0, h0 = 0;
           if (SPATIAL) {
@@ -527,7 +589,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t stage = 0, phase = 0;
       const int q = pt & 7;          // 16-byte piece index within a 128-byte row
       const int rsub = pt >> 3;      // rows rsub + 16 i
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
         const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
         int ih0[8], iw0[8];
         long long ioff[8];
@@ -630,12 +692,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t stage = 0, phase = 0, ast = 0, aph = 0;
       if (TMA_A && g.b_res) mbar_wait(bres, 0);
       int iter = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+      for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
         const int acc = iter & 1;
         const uint32_t acc_phase = (iter >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        if (MODE == 8) {
+          // 16 taps (r, s) of the 4x4 s2d stem, K = 16 each: A = the halo planes shifted by
+          // r*we + s pixels (16 B per pixel per plane), B = resident [tap][k half][n][8]
+          const uint32_t plane_stride = ((uint32_t)g.a_bytes / 2 + 127) / 128 * 128;
+          mbar_wait(&afull[ast], aph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_base = sA0 + ast * ASZ;
+#pragma unroll 1
+            for (int t = 0; t < 16; ++t) {
+              const int r = t >> 2, sft = t & 3;
+              const uint64_t adesc = make_sdesc_none(a_base + (uint32_t)(r * g.we + sft) * 16u, plane_stride, 128);
+              const uint64_t bdesc = make_sdesc_none(sB0 + t * 2048, 1024, 128);
+              mma_bf16(d_tmem, adesc, bdesc, idesc, t != 0);
+            }
+            mma_commit(&aempty[ast]);
+            mma_commit(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
+          continue;
+        }
         if (MODE == 6) {
           // tap (r, s) reads the halo shifted by r*we + s rows (the extra we - OW columns per
           // row are garbage rows of the tile, discarded by the epilogue)
@@ -719,7 +803,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // epilogue consumes them, into a 2-deep smem ring (TMA, same swizzle as the staging).
     if (g.has_res && lane == 0) {
       uint32_t rs = 0, rph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
         const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
         int w0 = 0, h0 = 0, b0 = 0;
         if (SPATIAL) tile_origin(g, tm, &w0, &h0, &b0);
@@ -752,7 +836,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t rs = 0, rph = 0;
     int blk = 0;
     int iter = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++iter) {
+    for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
       const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
@@ -765,6 +849,76 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      if (MODE == 8) {
+        // stem + 3x3/s2/p1 maxpool: relu(stem) rows -> smem ring of 3 stem rows (slot =
+        // stem row % 3), then pooled row po = max over stem rows 2po-1..2po+1.  Values are
+        // >= 0 after ReLU, so padding positions are written as 0.
+        const int W1 = 2 * g.pq + 1;
+        const int po = tm % g.ph, task = tm / g.ph;
+        const int n_img = task / g.strips, q0 = (task % g.strips) * g.pq;
+        uint8_t* ring = sY;  // 3 x W1 x 128 B (bf16 x 64 channels per stem pixel)
+        {
+          const int sr = row / g.we, sc = row - (row / g.we) * g.we;
+          const int stem_row = 2 * po + sr, stem_col = 2 * q0 - 1 + sc;
+          const bool live = sr < 2 && sc < W1;
+          const bool valid = live && stem_col >= 0 && stem_col < a.OW && stem_row < a.OH;
+          uint8_t* dst = ring + (((live ? stem_row : 0) % 3) * W1 + sc) * 128;
+#pragma unroll
+          for (int sub = gsel; sub < BN / 32; sub += 2) {
+            uint32_t v[32];
+            tmem_ld32(t_row + sub * 32, v);
+            tmem_wait_ld();
+            if (live) {
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                float f[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  f[j] = valid ? fmaxf(__uint_as_float(v[c4 * 8 + j]) + sBias[sub * 32 + c4 * 8 + j], 0.f) : 0.f;
+                uint4 o;
+                o.x = pack_bf16x2(f[0], f[1]);
+                o.y = pack_bf16x2(f[2], f[3]);
+                o.z = pack_bf16x2(f[4], f[5]);
+                o.w = pack_bf16x2(f[6], f[7]);
+                *reinterpret_cast<uint4*>(dst + (((sub * 4 + c4) ^ (sc & 7)) << 4)) = o;  // swizzled
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        epi_bar();
+        for (int it = et; it < g.pq * 8; it += NUM_EPI_THREADS) {
+          const int qo = it >> 3, cg = it & 7;
+          if (q0 + qo >= g.pw) continue;
+          float mx[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mx[j] = 0.f;
+          for (int dr = (po == 0 ? 1 : 0); dr < 3; ++dr) {
+            const uint8_t* rowp = ring + (((2 * po - 1 + dr + 3) % 3) * W1) * 128;
+#pragma unroll
+            for (int dc = 0; dc < 3; ++dc) {
+              const int col = 2 * qo + dc;
+              const uint4 u = *reinterpret_cast<const uint4*>(rowp + col * 128 + ((cg ^ (col & 7)) << 4));
+              const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float2 f2 = unpack_bf16x2(uu[j]);
+                mx[2 * j] = fmaxf(mx[2 * j], f2.x);
+                mx[2 * j + 1] = fmaxf(mx[2 * j + 1], f2.y);
+              }
+            }
+          }
+          uint4 o;
+          o.x = pack_bf16x2(mx[0], mx[1]);
+          o.y = pack_bf16x2(mx[2], mx[3]);
+          o.z = pack_bf16x2(mx[4], mx[5]);
+          o.w = pack_bf16x2(mx[6], mx[7]);
+          *reinterpret_cast<uint4*>(yb + (((long long)n_img * g.ph + po) * g.pw + q0 + qo) * a.y_ld + cg * 8) = o;
+        }
+        epi_bar();
+        continue;
+      }
       if (!g.tma_out) {
         // final layer straight into the NCHW send buffer (consecutive rows = consecutive
         // pixels, so thread-per-row stores are coalesced per channel)
@@ -896,14 +1050,19 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   int smem;
   const int res_bytes = g.has_res ? 2 * C::SB_BYTES : 0;
   const int bres_bytes = g.k_chunks * C::B_STAGE_BYTES;
-  const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 6;
+  const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 6 || g.mode == 8;
   const int a_min = g.mode == 6 ? g.a_stages * g.a_stage_bytes : 4 * A_STAGE_BYTES;
   // resident weights: measured win in halo mode; in modes 3/4 (e.g. the stem) it was slower
   g.b_res = tma_a && g.n_tiles == 1 && (g.mode == 6 || bres_enabled()) &&
             C::FIXED + res_bytes + a_min + bres_bytes <= SMEM_LIMIT;
   g.cps = (g.mode == 3 && BN <= 128) ? 2 : 1;
   const int pro_bytes = g.mode == 7 ? 8 * g.pro_c : 0;
-  if (g.mode == 6) {
+  if (g.mode == 8) {
+    g.b_res = 1;
+    g.stages = 2;  // B ring unused (placeholder for the barrier init loop)
+    smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED;
+    if (smem > SMEM_LIMIT) return cudaErrorInvalidValue;
+  } else if (g.mode == 6) {
     if (g.b_res) {
       g.stages = 1;  // B ring unused
       smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED + res_bytes;
@@ -924,7 +1083,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
     smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes + pro_bytes;
   }
   if (g.stages < 2 && !(g.mode == 6 && g.b_res)) return cudaErrorInvalidValue;
-  const int tiles = g.m_tiles * g.n_tiles;
+  const int tiles = g.mode == 8 ? g.n_tasks : g.m_tiles * g.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
   const CUtensorMap* b = mp.b;
@@ -941,6 +1100,9 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
     case 6: return launch_t<BN, 6>(a, g, mp, num_sms, st);
     case 7: return launch_t<BN, 7>(a, g, mp, num_sms, st);
+    case 8:
+      if (BN == 64) return launch_t<BN, 8>(a, g, mp, num_sms, st);
+      return cudaErrorInvalidValue;
   }
   return cudaErrorInvalidValue;
 }
@@ -978,7 +1140,31 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   g.n_tiles = (a.Cout + bn - 1) / bn;
   g.has_res = a.res != nullptr;
   g.tma_out = !a.nchw;
-  if (mode == 6) {
+  if (mode == 8) {
+    // stem conv (window view, KH=4 x 64 channels) fused with the 3x3/s2/p1 maxpool: a tile is
+    // 2 stem rows x (2 pq + 1) stem columns of one image strip; tasks = images x strips
+    if (a.Cout > 64 || a.C != BK || a.stride != 1) return cudaErrorInvalidValue;
+    g.pw = (a.OW - 1) / 2 + 1;
+    g.ph = (a.OH - 1) / 2 + 1;
+    g.strips = (g.pw + 30) / 31;
+    g.pq = (g.pw + g.strips - 1) / g.strips;
+    g.n_tasks = a.N * g.strips;
+    g.wb = 2 * g.pq + 1; g.hb = 2; g.nb = 1;
+    g.we = g.wb + 3;                          // 4x4 taps over the padded s2d map
+    if (2 * g.we > BM) return cudaErrorInvalidValue;
+    g.tiles_w = 1; g.tiles_h = 1;
+    g.m_tiles = g.n_tasks * g.ph;
+    g.cblocks = 1;
+    g.k_chunks = a.KH * a.KW;                 // 4 x 64 = 256 = 16 taps x 16 (resident B size)
+    g.a_bytes = 2 * (16 * g.we * 5);          // two planes of 5 rows x we pixels x 16 B
+    {
+      const int plane_stride = (g.a_bytes / 2 + 127) / 128 * 128;
+      const int rows_read = BM + 3 * g.we + 3;  // by the last tap (rows past the box: garbage rows)
+      g.a_stage_bytes = (plane_stride + rows_read * 16 + 1023) / 1024 * 1024;
+    }
+    g.a_stages = MAX_A_STAGES;
+    g.tma_out = 0;
+  } else if (mode == 6) {
     // halo tile: full output rows (wb = OW), hb rows, one image; extended width we = OW + KW - 1
     if (a.stride != 1 || a.C % BK != 0) return cudaErrorInvalidValue;
     g.we = a.OW + a.KW - 1;
@@ -992,7 +1178,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     const int rows_read = (a.KH - 1) * g.we + (a.KW - 1) + BM;   // by the last tap's MMA
     const int rows = rows_read > g.a_bytes / 128 ? rows_read : g.a_bytes / 128;
     g.a_stage_bytes = (rows * 128 + 1023) / 1024 * 1024;
-    g.a_stages = MAX_A_STAGES;
+    g.a_stages = 2;
   } else if (mode == 4) {
     g.wb = wb; g.hb = hb; g.nb = nb;
     g.tiles_w = (a.OW + wb - 1) / wb;
@@ -1018,7 +1204,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     if ((mode != 3 && mode != 4) || !mp.a2) return cudaErrorInvalidValue;
     g.k_chunks += a.k2_chunks;
   }
-  if ((mode == 3 || mode == 4 || mode == 6) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
+  if ((mode == 3 || mode == 4 || mode == 6 || mode == 8) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
   if (g.tma_out && !mp.y) return cudaErrorInvalidValue;
   if (g.has_res && g.tma_out && !mp.r) return cudaErrorInvalidValue;
   if (g.has_res && !g.tma_out) g.has_res = 0;  // NCHW path reads the residual directly

@@ -70,6 +70,14 @@ bool prologue_tma_enabled() {
   return on;
 }
 
+bool stem_pool_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_STEM_POOL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool halo_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_HALO");
@@ -92,6 +100,7 @@ struct ConvW {
   int cout = 0, kh = 1, kw = 1, stride = 1, pad = 0;
   int K = 0, Kp = 0;
   void* w = nullptr;           // bf16 [Cout][Kp] (tc) or fp32 [K][Cout] (simt)
+  void* w8 = nullptr;          // s2d stem, mode 8: bf16 [tap 16][k half 2][n 64][8] (no-swizzle K-major)
   float* bias = nullptr;       // [Cout]
   float* pro_scale = nullptr;  // [cs]
   float* pro_shift = nullptr;
@@ -123,6 +132,7 @@ struct Op {
   int wb = 0, hb = 0, nb = 0;    // mode 4 spatial tile
   int layout = 0;                // pack_in layout
   bool s2d_view = false;         // stem over the padded space-to-depth window view
+  int conv_oh = 0, conv_ow = 0;  // mode 8: stem map size (out is the pooled map)
   CUtensorMap tmap_a;            // modes 3/4 (built after the arena is placed)
   CUtensorMap tmap_y;            // NHWC output view (TMA-store epilogue)
   CUtensorMap tmap_r;            // residual view
@@ -342,6 +352,18 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     hapi_status st = upload(m, hw, &dw);
     if (st != HAPI_OK) return st;
     cw.w = dw;
+    if (s.s2d && s.cout <= 64) {
+      // one 16-channel tap per MMA (K = 16): [tap][k half][n][8] = core matrices of 8 n x 16 B
+      std::vector<uint16_t> h8((size_t)taps * 2 * 64 * 8, 0);
+      for (int tap = 0; tap < taps; ++tap)
+        for (int kh = 0; kh < 2; ++kh)
+          for (int o = 0; o < s.cout; ++o)
+            for (int j = 0; j < 8; ++j)
+              h8[(((size_t)tap * 2 + kh) * 64 + o) * 8 + j] = hw[(size_t)o * cw.Kp + tap * 16 + kh * 8 + j];
+      uint16_t* d8;
+      if ((st = upload(m, h8, &d8)) != HAPI_OK) return st;
+      cw.w8 = d8;
+    }
     cw.bn = conv_tc_pick_bn(s.cout);
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -538,7 +560,29 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         cs.cs = cur.C;
         cs.s2d = (i == 0 && s2d);
         const int ih = cs.s2d ? H0 : cur.H, iw = cs.s2d ? W0 : cur.W;
-        View o = b.compact(md.cout, out_dim(ih, md.k, md.stride, md.pad), out_dim(iw, md.k, md.stride, md.pad));
+        const int oh = out_dim(ih, md.k, md.stride, md.pad), ow = out_dim(iw, md.k, md.stride, md.pad);
+        const int jp = j + (relu ? 1 : 0);
+        if (cs.s2d && relu && md.cout <= 64 && jp < split && mods[jp].kind == MK_MAXPOOL && mods[jp].k == 3 &&
+            mods[jp].stride == 2 && mods[jp].pad == 1 && stem_pool_enabled()) {
+          // stem conv + bn + relu + 3x3/s2/p1 maxpool in one kernel (tcgen05 mode 8): the stem
+          // map never reaches HBM
+          View o = b.compact(md.cout, out_dim(oh, 3, 2, 1), out_dim(ow, 3, 2, 1));
+          Op* op = nullptr;
+          if ((st = b.conv(cs, cur, o, relu, nullptr, &op)) != HAPI_OK) return st;
+          if (!m->convs[op->conv].w8) return set_error(HAPI_ERR_UNSUPPORTED, "stem weights for mode 8 missing");
+          op->tc_mode = 8;
+          op->conv_oh = oh; op->conv_ow = ow;
+          const int pw = o.W, strips = (pw + 30) / 31, pq = (pw + strips - 1) / strips;
+          op->wb = 2 * pq + 1; op->hb = 2; op->nb = 1;
+          const ConvW& w = m->convs[op->conv];
+          op->flops = w.real_flops_per_px * (double)oh * ow;
+          op->bytes = ((double)cur.H * cur.W * cur.C + (double)o.H * o.W * o.C) * m->es;
+          op->desc += " +maxpool3/s2 mode8";
+          cur = o;
+          i = jp + 1;
+          break;
+        }
+        View o = b.compact(md.cout, oh, ow);
         if ((st = b.conv(cs, cur, o, relu, nullptr)) != HAPI_OK) return st;
         cur = o;
         i = j + (relu ? 1 : 0);
@@ -758,7 +802,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   const bool compact = cur.ld == cur.C && cur.coff == 0;
   const bool same_view = cur.buf >= 0 && last.out.buf == cur.buf && last.out.C == cur.C && last.out.ld == cur.ld &&
                          last.out.coff == cur.coff;
-  const bool can_direct = same_view && compact && last.t != OP_PACK_IN;
+  const bool can_direct = same_view && compact && last.t != OP_PACK_IN && !(last.t == OP_CONV && last.tc_mode == 8);
   if (can_direct && last.t == OP_CONV) {
     last.out.buf = -1;
     last.nchw_out = true;
@@ -860,6 +904,11 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.stride2 = w.stride2;
       if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
         a.C = 64; a.KH = 4; a.KW = 1; a.stride = 1; a.pad = 0;
+      }
+      if (o.tc_mode == 8) {  // the kernel iterates the stem map; y is the pooled map
+        a.OH = o.conv_oh; a.OW = o.conv_ow;
+        a.w = w.w8;
+        a.M = (long long)nb * a.OH * a.OW;
       }
       if (m->bf16) {
         ConvMaps mp;
@@ -971,12 +1020,24 @@ hapi_status finalize_tmaps(hapi_model* m) {
       if (o.t != OP_CONV) continue;
       const ConvW& w = m->convs[o.conv];
       hapi_status st = HAPI_OK;
-      if (o.s2d_view) {
+      if (o.tc_mode == 8) {
+        // halo box over the padded s2d input [N][HP][WP][16]: {8 channels, wb + 3, 2 + 3, 1},
+        // loaded twice (channels 0-7, 8-15) into two 16-byte-per-pixel planes
+        void* base = vptr(m, p, o.in, nullptr);
+        const cuuint64_t px = (cuuint64_t)o.in.ld * 2;
+        cuuint64_t dims[4] = {16, (cuuint64_t)o.in.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+        cuuint64_t strides[3] = {px, px * o.in.W, px * o.in.W * o.in.H};
+        cuuint32_t box[4] = {8, (cuuint32_t)(o.wb + 3), 5, 1};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_NONE, o.desc + " stem halo");
+        if (st != HAPI_OK) return st;
+      } else if (o.s2d_view) {
         // overlapping window view of the padded s2d input: element (e, w, h, n) at
         // base + n*HP*WP*32 + h*WP*32 + w*32 + 2e, e < 64 spans 4 adjacent pixels
         void* base = vptr(m, p, o.in, nullptr);
         const cuuint64_t px = (cuuint64_t)o.in.ld * 2;  // 32 B
-        cuuint64_t dims[4] = {64, (cuuint64_t)o.out.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+        const int stem_w = o.tc_mode == 8 ? o.conv_ow : o.out.W;
+        cuuint64_t dims[4] = {64, (cuuint64_t)stem_w, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
         cuuint64_t strides[3] = {px, px * o.in.W, px * o.in.W * o.in.H};
         cuuint32_t box[4] = {64, (cuuint32_t)o.wb, (cuuint32_t)o.hb, (cuuint32_t)o.nb};
         cuuint32_t estr[4] = {1, 1, 1, 1};
@@ -1030,7 +1091,7 @@ hapi_status finalize_tmaps(hapi_model* m) {
         }
         if (st != HAPI_OK) return st;
       }
-      if (!o.nchw_out) {
+      if (!o.nchw_out && o.tc_mode != 8) {
         const int cols = conv_tc_store_cols(w.bn);
         if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y")) != HAPI_OK) return st;
         if (o.has_res && (st = encode_view(m, p, o, o.res, cols, &o.tmap_r, "R")) != HAPI_OK) return st;
