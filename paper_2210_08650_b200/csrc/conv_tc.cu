@@ -48,6 +48,9 @@ constexpr int MMA_WARP = 12;
 constexpr int RES_WARP = 13;
 constexpr int XFORM_TMA_WARP = 14;   // mode 7: TMA issuer while warps 8-11 transform
 constexpr int NUM_THREADS = 15 * 32;
+constexpr int M8_POOL_WARP0 = 9;      // mode 8: warps 9-11 pool while 0-7 drain TMEM
+constexpr int M8_POOL_THREADS = 96;
+constexpr int M8_RING = 6;            // mode 8: stem rows held in smem (tile i: rows 2i, 2i+1)
 constexpr int A_STAGE_BYTES = BM * BK * 2;
 constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in per CTA
 constexpr int MAX_STAGES = 8;
@@ -65,7 +68,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 1024 /*barriers*/;
-  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 9) * 8 + 4 <= 1024, "barrier area");
+  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 13) * 8 + 4 <= 1024, "barrier area");
   static int stages(bool res) {
     int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
     return s > MAX_STAGES ? MAX_STAGES : s;
@@ -227,6 +230,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// relu + round to bf16x2 in one instruction: low half <- lo, high half <- hi
+__device__ __forceinline__ uint32_t cvt_relu_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+__device__ __forceinline__ uint32_t bf16x2_max(uint32_t x, uint32_t y) {
+  __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&x), b = *reinterpret_cast<__nv_bfloat162*>(&y);
+  __nv_bfloat162 r = __hmax2(a, b);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
 __device__ __forceinline__ float2 unpack_bf16x2(uint32_t u) {
   __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&u);
   return __bfloat1622float2(h);
@@ -250,6 +264,7 @@ struct Geo {
   int cps;                     // K chunks per pipeline stage (modes 3/4: 2 when BN <= 128)
   int pro_c;                   // mode 7: channels of the smem scale/shift tables (C rounded to 64)
   int ph, pw, pq, strips, n_tasks;  // mode 8: pooled map, pool columns per strip, strips/image, tasks
+  int ring_bytes;                   // mode 8: M8_RING stem rows x (2 pq + 1) pixels x 128 B
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -337,7 +352,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + AS * ASZ;
   uint8_t* sY = sB + (g.b_res ? g.k_chunks * C::B_STAGE_BYTES : S * BSZ);  // 2 output staging blocks
-  uint8_t* sR = sY + 2 * C::SB_BYTES;                      // 2 residual blocks (if has_res)
+  uint8_t* sR = sY + (MODE == 8 ? g.ring_bytes : 2 * C::SB_BYTES);  // 2 residual blocks (if has_res)
   float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? 2 * C::SB_BYTES : 0));
   float* sScale = sBias + BN;                                   // mode 7 prologue tables
   float* sShift = sScale + (MODE == 7 ? g.pro_c : 0);
@@ -351,7 +366,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* rempty = rfull + 2;
   uint64_t* bres = rempty + 2;               // resident weights landed
   uint64_t* lfull = bres + 1;                // mode 7: raw A tile landed (before the transform)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lfull + MAX_B_STAGES);
+  uint64_t* pready = lfull + MAX_B_STAGES;   // mode 8: stem rows of a tile in the ring
+  uint64_t* pfree = pready + 2;              // mode 8: pooling of a tile done (its ring rows free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfree + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -374,6 +391,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&rempty[i], NUM_EPI_THREADS);
     }
     mbar_init(bres, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&pready[i], NUM_EPI_THREADS);
+      mbar_init(&pfree[i], M8_POOL_THREADS);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == PROD_WARP0 && lane == 0) {
@@ -463,6 +484,107 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
       }
     }
+  } else if (MODE == 8 && warp >= M8_POOL_WARP0 && warp < PROD_WARP0 + 4) {
+    // ================================================================ mode 8 pooling
+    // 3x3/s2/p1 max over the ring: pooled row po of a strip = max over stem rows 2po-1..2po+1
+    // (ring rows 2i-1, 2i, 2i+1 of local tile i; at po = 0 row 2i stands in for the missing
+    // row -1 -- values are >= 0 after ReLU and max is idempotent).  Item = (pooled column,
+    // 8-channel group); 16-byte swizzled smem reads, one 16-byte global store.
+    const int pt = threadIdx.x - M8_POOL_WARP0 * 32;
+    const int rowbytes = (2 * g.pq + 1) * 128;
+    const uint32_t ring = smem_u32(sY);
+    __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.y);
+    int po = 0, task = blockIdx.x, img = task / g.strips, q0 = (task - img * g.strips) * g.pq, kslot = 0;
+    for (int it = 0; task < g.n_tasks; ++it) {
+      mbar_wait(&pready[it & 1], (it >> 1) & 1);
+      const int r0 = 2 * kslot, r1 = r0 + 1, rp = po == 0 ? r0 : (r0 == 0 ? M8_RING - 1 : r0 - 1);
+      const uint32_t b0 = ring + rp * rowbytes, b1 = ring + r0 * rowbytes, b2 = ring + r1 * rowbytes;
+      for (int item = pt; item < g.pq * 8; item += M8_POOL_THREADS) {
+        const int qo = item >> 3, cg = item & 7;
+        if (q0 + qo >= g.pw) continue;
+        uint32_t mx[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int dc = 0; dc < 3; ++dc) {
+          const int col = 2 * qo + dc;
+          const uint32_t off = (uint32_t)(col * 128 + ((cg ^ (col & 7)) << 4));
+          const uint32_t rb[3] = {b0, b1, b2};
+#pragma unroll
+          for (int dr = 0; dr < 3; ++dr) {
+            uint32_t u[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                         : "r"(rb[dr] + off));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mx[j] = bf16x2_max(mx[j], u[j]);
+          }
+        }
+        *reinterpret_cast<uint4*>(yb + (((long long)img * g.ph + po) * g.pw + q0 + qo) * a.y_ld + cg * 8) =
+            make_uint4(mx[0], mx[1], mx[2], mx[3]);
+      }
+      mbar_arrive(&pfree[it & 1]);
+      kslot = kslot == M8_RING / 2 - 1 ? 0 : kslot + 1;
+      if (++po == g.ph) {
+        po = 0;
+        task += gridDim.x;
+        img = task / g.strips;
+        q0 = (task - img * g.strips) * g.pq;
+      }
+    }
+  } else if (MODE == 8 && warp < NUM_EPI_WARPS) {
+    // ================================================================ mode 8 epilogue
+    // TMEM -> + bias (registers) -> ReLU -> bf16 -> the two stem rows of the tile into ring
+    // rows 2i, 2i+1 (swizzled 16-byte chunks), then signal the pooling warps.  Runs one tile
+    // ahead of the pooling: tile i reuses the ring rows of tile i-3, pooled by tile i-2 at
+    // the latest (pfree).
+    const int quarter = warp & 3, gsel = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int sr = row / g.we, sc = row - sr * g.we;
+    const bool live = sr < 2 && sc < 2 * g.pq + 1;
+    const int rowbytes = (2 * g.pq + 1) * 128;
+    const uint32_t ring = smem_u32(sY) + (uint32_t)(sr * rowbytes + sc * 128);
+    float bias[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int n = gsel * 32 + j;
+      bias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
+    }
+    int po = 0, task = blockIdx.x, q0 = (task % g.strips) * g.pq, kslot = 0;
+    for (int it = 0; task < g.n_tasks; ++it) {
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      mbar_wait(&pfree[it & 1], ((it >> 1) & 1) ^ 1);
+      const int stem_row = 2 * po + sr, stem_col = 2 * q0 - 1 + sc;
+      const bool valid = live && stem_col >= 0 && stem_col < a.OW && stem_row < a.OH;
+      uint32_t v[32];
+      tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + gsel * 32, v);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (live) {
+        const uint32_t dst = ring + (uint32_t)(2 * kslot * rowbytes);
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          uint32_t o[4] = {0u, 0u, 0u, 0u};
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              o[j] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * j]) + bias[c4 * 8 + 2 * j],
+                                     __uint_as_float(v[c4 * 8 + 2 * j + 1]) + bias[c4 * 8 + 2 * j + 1]);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (((gsel * 4 + c4) ^ (sc & 7)) << 4)),
+                       "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                       : "memory");
+        }
+      }
+      mbar_arrive(&pready[it & 1]);
+      kslot = kslot == M8_RING / 2 - 1 ? 0 : kslot + 1;
+      if (++po == g.ph) {
+        po = 0;
+        task += gridDim.x;
+        q0 = (task % g.strips) * g.pq;
+      }
+    }
   } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ producer
     const int pt = threadIdx.x - PROD_WARP0 * 32;
@@ -477,7 +599,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     if (MODE == 8) {
       // stem halo: resident weights once, then per tile one [5 rows x we] box of the padded
-      // s2d input as two 16-byte-per-pixel planes (channels 0-7 | 8-15)
+      // s2d input as two 16-byte-per-pixel planes (channels 0-7 | 8-15).  (A single
+      // 32-byte-swizzled box read through SW32 descriptors is correct too but measured
+      // slower: 0.43 vs 0.37 ms for ResNet-50 b512.)
       if (warp == PROD_WARP0) {
         if (elect_one()) {
           mbar_arrive_expect_tx(bres, 16 * 2 * 64 * 16);
@@ -485,8 +609,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         __syncwarp();
         uint32_t ast = 0, aph = 0;
-        const uint32_t plane = (uint32_t)g.a_bytes / 2;
-        const uint32_t plane_stride = (plane + 127) / 128 * 128;
+        const uint32_t plane_stride = ((uint32_t)g.a_bytes / 2 + 127) / 128 * 128;
         for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
           int w0, h0, b0;
           tile_origin(g, tile, &w0, &h0, &b0);
@@ -700,7 +823,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t d_tmem = tmem_base + acc * BN;
         if (MODE == 8) {
           // 16 taps (r, s) of the 4x4 s2d stem, K = 16 each: A = the halo planes shifted by
-          // r*we + s pixels (16 B per pixel per plane), B = resident [tap][k half][n][8]
+          // r*we + s pixels (16 B per pixel per plane), B = resident [tap][k half][n][8].
+          // N = 64 MMAs are smem-bandwidth bound (48 cycles measured vs 32 floor:
+          // tools/micro/mma_rate.cu), and the epilogue/pooling smem traffic shares that port.
           const uint32_t plane_stride = ((uint32_t)g.a_bytes / 2 + 127) / 128 * 128;
           mbar_wait(&afull[ast], aph);
           tc_fence_after();
@@ -849,76 +974,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      if (MODE == 8) {
-        // stem + 3x3/s2/p1 maxpool: relu(stem) rows -> smem ring of 3 stem rows (slot =
-        // stem row % 3), then pooled row po = max over stem rows 2po-1..2po+1.  Values are
-        // >= 0 after ReLU, so padding positions are written as 0.
-        const int W1 = 2 * g.pq + 1;
-        const int po = tm % g.ph, task = tm / g.ph;
-        const int n_img = task / g.strips, q0 = (task % g.strips) * g.pq;
-        uint8_t* ring = sY;  // 3 x W1 x 128 B (bf16 x 64 channels per stem pixel)
-        {
-          const int sr = row / g.we, sc = row - (row / g.we) * g.we;
-          const int stem_row = 2 * po + sr, stem_col = 2 * q0 - 1 + sc;
-          const bool live = sr < 2 && sc < W1;
-          const bool valid = live && stem_col >= 0 && stem_col < a.OW && stem_row < a.OH;
-          uint8_t* dst = ring + (((live ? stem_row : 0) % 3) * W1 + sc) * 128;
-#pragma unroll
-          for (int sub = gsel; sub < BN / 32; sub += 2) {
-            uint32_t v[32];
-            tmem_ld32(t_row + sub * 32, v);
-            tmem_wait_ld();
-            if (live) {
-#pragma unroll
-              for (int c4 = 0; c4 < 4; ++c4) {
-                float f[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  f[j] = valid ? fmaxf(__uint_as_float(v[c4 * 8 + j]) + sBias[sub * 32 + c4 * 8 + j], 0.f) : 0.f;
-                uint4 o;
-                o.x = pack_bf16x2(f[0], f[1]);
-                o.y = pack_bf16x2(f[2], f[3]);
-                o.z = pack_bf16x2(f[4], f[5]);
-                o.w = pack_bf16x2(f[6], f[7]);
-                *reinterpret_cast<uint4*>(dst + (((sub * 4 + c4) ^ (sc & 7)) << 4)) = o;  // swizzled
-              }
-            }
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        epi_bar();
-        for (int it = et; it < g.pq * 8; it += NUM_EPI_THREADS) {
-          const int qo = it >> 3, cg = it & 7;
-          if (q0 + qo >= g.pw) continue;
-          float mx[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) mx[j] = 0.f;
-          for (int dr = (po == 0 ? 1 : 0); dr < 3; ++dr) {
-            const uint8_t* rowp = ring + (((2 * po - 1 + dr + 3) % 3) * W1) * 128;
-#pragma unroll
-            for (int dc = 0; dc < 3; ++dc) {
-              const int col = 2 * qo + dc;
-              const uint4 u = *reinterpret_cast<const uint4*>(rowp + col * 128 + ((cg ^ (col & 7)) << 4));
-              const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const float2 f2 = unpack_bf16x2(uu[j]);
-                mx[2 * j] = fmaxf(mx[2 * j], f2.x);
-                mx[2 * j + 1] = fmaxf(mx[2 * j + 1], f2.y);
-              }
-            }
-          }
-          uint4 o;
-          o.x = pack_bf16x2(mx[0], mx[1]);
-          o.y = pack_bf16x2(mx[2], mx[3]);
-          o.z = pack_bf16x2(mx[4], mx[5]);
-          o.w = pack_bf16x2(mx[6], mx[7]);
-          *reinterpret_cast<uint4*>(yb + (((long long)n_img * g.ph + po) * g.pw + q0 + qo) * a.y_ld + cg * 8) = o;
-        }
-        epi_bar();
-        continue;
-      }
       if (!g.tma_out) {
         // final layer straight into the NCHW send buffer (consecutive rows = consecutive
         // pixels, so thread-per-row stores are coalesced per channel)
@@ -1060,7 +1115,8 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   if (g.mode == 8) {
     g.b_res = 1;
     g.stages = 2;  // B ring unused (placeholder for the barrier init loop)
-    smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED;
+    const int ring_extra = g.ring_bytes > 2 * C::SB_BYTES ? g.ring_bytes - 2 * C::SB_BYTES : 0;
+    smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED + ring_extra;
     if (smem > SMEM_LIMIT) return cudaErrorInvalidValue;
   } else if (g.mode == 6) {
     if (g.b_res) {
@@ -1163,6 +1219,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
       g.a_stage_bytes = (plane_stride + rows_read * 16 + 1023) / 1024 * 1024;
     }
     g.a_stages = MAX_A_STAGES;
+    g.ring_bytes = (M8_RING * g.wb * 128 + 1023) / 1024 * 1024;
     g.tma_out = 0;
   } else if (mode == 6) {
     // halo tile: full output rows (wb = OW), hb rows, one image; extended width we = OW + KW - 1
