@@ -56,6 +56,7 @@ constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in pe
 constexpr int MAX_STAGES = 8;
 constexpr int MAX_B_STAGES = 16;  // mode 6 weight ring
 constexpr int MAX_A_STAGES = 8;   // mode 6 / mode 8 halo rings
+constexpr int MAX_RES = 8;        // residual ring depth
 
 // Static part of the shared-memory carve-up; the pipeline depth is chosen per launch.
 template <int BN>
@@ -68,7 +69,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 1024 /*barriers*/;
-  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 13) * 8 + 4 <= 1024, "barrier area");
+  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 2 * MAX_RES + 9) * 8 + 4 <= 1024, "barrier area");
   static int stages(bool res) {
     int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
     return s > MAX_STAGES ? MAX_STAGES : s;
@@ -265,6 +266,7 @@ struct Geo {
   int pro_c;                   // mode 7: channels of the smem scale/shift tables (C rounded to 64)
   int ph, pw, pq, strips, n_tasks;  // mode 8: pooled map, pool columns per strip, strips/image, tasks
   int ring_bytes;                   // mode 8: M8_RING stem rows x (2 pq + 1) pixels x 128 B
+  int res_depth;                    // residual ring depth (blocks of [128 x SB] in flight)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -352,8 +354,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + AS * ASZ;
   uint8_t* sY = sB + (g.b_res ? g.k_chunks * C::B_STAGE_BYTES : S * BSZ);  // 2 output staging blocks
-  uint8_t* sR = sY + (MODE == 8 ? g.ring_bytes : 2 * C::SB_BYTES);  // 2 residual blocks (if has_res)
-  float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? 2 * C::SB_BYTES : 0));
+  uint8_t* sR = sY + (MODE == 8 ? g.ring_bytes : 2 * C::SB_BYTES);  // residual ring (if has_res)
+  float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? g.res_depth * C::SB_BYTES : 0));
   float* sScale = sBias + BN;                                   // mode 7 prologue tables
   float* sShift = sScale + (MODE == 7 ? g.pro_c : 0);
   uint64_t* full = reinterpret_cast<uint64_t*>(sShift + (MODE == 7 ? g.pro_c : 0));
@@ -363,8 +365,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = aempty + MAX_A_STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* rfull = tempty + 2;
-  uint64_t* rempty = rfull + 2;
-  uint64_t* bres = rempty + 2;               // resident weights landed
+  uint64_t* rempty = rfull + MAX_RES;
+  uint64_t* bres = rempty + MAX_RES;         // resident weights landed
   uint64_t* lfull = bres + 1;                // mode 7: raw A tile landed (before the transform)
   uint64_t* pready = lfull + MAX_B_STAGES;   // mode 8: stem rows of a tile in the ring
   uint64_t* pfree = pready + 2;              // mode 8: pooling of a tile done (its ring rows free)
@@ -387,6 +389,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], NUM_EPI_THREADS);
+    }
+    for (int i = 0; i < MAX_RES; ++i) {
       mbar_init(&rfull[i], 1);
       mbar_init(&rempty[i], NUM_EPI_THREADS);
     }
@@ -942,7 +946,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tma_load_4d(dst, &tmap_r, n0, w0, h0, b0, &rfull[rs]);
           else
             tma_load_2d(dst, &tmap_r, n0, tm * BM, &rfull[rs]);
-          if (++rs == 2) { rs = 0; rph ^= 1; }
+          if (++rs == (uint32_t)g.res_depth) { rs = 0; rph ^= 1; }
         }
       }
     }
@@ -1054,7 +1058,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           if (g.has_res) {
             mbar_arrive(&rempty[rs]);
-            if (++rs == 2) { rs = 0; rph ^= 1; }
+            if (++rs == (uint32_t)g.res_depth) { rs = 0; rph ^= 1; }
           }
           fence_proxy_async_smem();
           epi_bar();
@@ -1091,6 +1095,22 @@ bool bres_enabled() {  // HAPI_BRES=1: also keep weights resident in modes 3/4 (
   return on;
 }
 
+// Residual ring depth: the deepest ring that costs no pipeline stage (measured on ResNet-50
+// b512: depth 3 beats 2 by 8% on the +res convs; depth 4/6 lose a BN=256 stage and are slower).
+// HAPI_RES_DEPTH overrides.
+int res_depth_pick(int stage_bytes, int fixed, int sb_bytes) {
+  static const int forced = [] {
+    const char* e = std::getenv("HAPI_RES_DEPTH");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced) return forced < 2 ? 2 : (forced > MAX_RES ? MAX_RES : forced);
+  auto stages = [&](int d) { return (SMEM_LIMIT - fixed - d * sb_bytes) / stage_bytes; };
+  const int s2 = stages(2) > MAX_STAGES ? MAX_STAGES : stages(2);
+  int d = 2;
+  while (d < MAX_RES && stages(d + 1) >= s2) ++d;
+  return d;
+}
+
 template <int BN, int MODE>
 cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, cudaStream_t st) {
   using C = Cfg<BN>;
@@ -1103,14 +1123,15 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   }
   g.res_box_bytes = (g.mode == 4 || g.mode == 6) ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
   int smem;
-  const int res_bytes = g.has_res ? 2 * C::SB_BYTES : 0;
+  g.cps = (g.mode == 3 && BN <= 128) ? 2 : 1;
+  g.res_depth = res_depth_pick(g.cps * C::STAGE_BYTES, C::FIXED, C::SB_BYTES);
+  const int res_bytes = g.has_res ? g.res_depth * C::SB_BYTES : 0;
   const int bres_bytes = g.k_chunks * C::B_STAGE_BYTES;
   const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 6 || g.mode == 8;
   const int a_min = g.mode == 6 ? g.a_stages * g.a_stage_bytes : 4 * A_STAGE_BYTES;
   // resident weights: measured win in halo mode; in modes 3/4 (e.g. the stem) it was slower
   g.b_res = tma_a && g.n_tiles == 1 && (g.mode == 6 || bres_enabled()) &&
             C::FIXED + res_bytes + a_min + bres_bytes <= SMEM_LIMIT;
-  g.cps = (g.mode == 3 && BN <= 128) ? 2 : 1;
   const int pro_bytes = g.mode == 7 ? 8 * g.pro_c : 0;
   if (g.mode == 8) {
     g.b_res = 1;
