@@ -267,6 +267,7 @@ struct Geo {
   int ph, pw, pq, strips, n_tasks;  // mode 8: pooled map, pool columns per strip, strips/image, tasks
   int ring_bytes;                   // mode 8: M8_RING stem rows x (2 pq + 1) pixels x 128 B
   int res_depth;                    // residual ring depth (blocks of [128 x SB] in flight)
+  int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -342,12 +343,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 6 || MODE == 7 || MODE == 8);
-  constexpr bool SPATIAL = (MODE == 4 || MODE == 6 || MODE == 8);
+  // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
+  constexpr bool HALO = (MODE == 6 || MODE == 9);
+  constexpr int MT = MODE == 9 ? 2 : 1;
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || HALO || MODE == 7 || MODE == 8);
+  constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   const int S = g.stages;
-  const int AS = (MODE == 6 || MODE == 8) ? g.a_stages : S;
+  const int AS = (HALO || MODE == 8) ? g.a_stages : S;
   constexpr int CPS = (MODE == 3 && BN <= 128) ? 2 : 1;  // == g.cps (host); mode 4 measured better at 1
-  const int ASZ = (MODE == 6 || MODE == 8) ? g.a_stage_bytes : CPS * A_STAGE_BYTES;   // A ring slot
+  const int ASZ = HALO ? MT * g.a_stage_bytes : MODE == 8 ? g.a_stage_bytes : CPS * A_STAGE_BYTES;  // A slot
   const int BSZ = CPS * C::B_STAGE_BYTES;                               // B ring slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C::TMEM_COLS)
+                 "r"(C::TMEM_COLS * MT)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();  // the previous kernel's outputs are visible from here on
 
-  const int num_tiles = g.m_tiles * g.n_tiles;
+  const int num_tiles = (g.m_tiles + MT - 1) / MT * g.n_tiles;
   const int OHW = a.OH * a.OW;
 
   if (MODE == 7 && warp == XFORM_TMA_WARP) {
@@ -628,20 +632,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
         }
       }
-    } else if (MODE == 6) {
+    } else if (HALO) {
       // halo mode: one [(hb+KH-1) x we] pixel box per 64-channel block, then the taps' weights
       if (warp == PROD_WARP0) {
         uint32_t stage = 0, phase = 0, ast = 0, aph = 0;
         const int taps = a.KH * a.KW;
         for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
-          const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
-          int ow0, oh0, b0;
-          tile_origin(g, tm, &ow0, &oh0, &b0);
+          const int tm0 = (tile / g.n_tiles) * MT, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+          const int nsub = g.m_tiles - tm0 < MT ? g.m_tiles - tm0 : MT;
           for (int cb = 0; cb < g.cblocks; ++cb) {
             mbar_wait(&aempty[ast], aph ^ 1);
             if (elect_one()) {
-              mbar_arrive_expect_tx(&afull[ast], g.a_bytes);
-              tma_load_4d(smem_u32(sA + ast * ASZ), &tmap_a, cb * BK, ow0 - a.pad, oh0 - a.pad, b0, &afull[ast]);
+              // one halo box per M sub-tile (they share every B stage below)
+              mbar_arrive_expect_tx(&afull[ast], g.a_bytes * nsub);
+              for (int sub = 0; sub < nsub; ++sub) {
+                int ow0, oh0, b0;
+                tile_origin(g, tm0 + sub, &ow0, &oh0, &b0);
+                tma_load_4d(smem_u32(sA + ast * ASZ + sub * g.a_stage_bytes), &tmap_a, cb * BK, ow0 - a.pad,
+                            oh0 - a.pad, b0, &afull[ast]);
+              }
             }
             __syncwarp();
             if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
@@ -849,26 +858,42 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
           continue;
         }
-        if (MODE == 6) {
+        if (HALO) {
           // tap (r, s) reads the halo shifted by r*we + s rows (the extra we - OW columns per
-          // row are garbage rows of the tile, discarded by the epilogue)
-          const int taps = a.KH * a.KW;
+          // row are garbage rows of the tile, discarded by the epilogue).  With mt = 2 every B
+          // stage feeds the MMAs of two M sub-tiles (halves the weight traffic from L2).
+          const int tm0 = (tile / g.n_tiles) * MT;
+          const int nsub = g.m_tiles - tm0 < MT ? g.m_tiles - tm0 : MT;
+          const uint32_t d_base = tmem_base + acc * MT * BN;
           uint32_t accum = 0;
           for (int cb = 0; cb < g.cblocks; ++cb) {
             mbar_wait(&afull[ast], aph);
             tc_fence_after();
             const uint32_t a_base = sA0 + ast * ASZ;
+            // descriptors built once per channel block and advanced by adds (start-address
+            // field in 16-byte units): tap (r, s) = + (r*we + s) * 8, next K16 step = + 2
+            const uint64_t a0 = make_sdesc(a_base);
+            const uint64_t a1 = make_sdesc(a_base + (MT > 1 ? g.a_stage_bytes : 0));
+            const uint32_t rstep = (uint32_t)g.we * 8u;
             if (g.b_res) {
               // weights resident: all taps of this channel block in one burst
               if (elect_one()) {
-                int r = 0, sft = 0;
-                for (int t = 0; t < taps; ++t) {
-                  const uint64_t adesc = make_sdesc_rows(a_base, r * g.we + sft);
-                  const uint64_t bdesc = make_sdesc(sB0 + (t * g.cblocks + cb) * C::B_STAGE_BYTES);
+                uint64_t bd = make_sdesc(sB0 + cb * C::B_STAGE_BYTES);
+                const uint32_t bstep = (uint32_t)(g.cblocks * C::B_STAGE_BYTES) >> 4;
+                uint32_t roff = 0;
+                for (int r = 0; r < a.KH; ++r, roff += rstep) {
+                  for (int sft = 0; sft < a.KW; ++sft, bd += bstep) {
+                    const uint32_t off = roff + (uint32_t)sft * 8u;
+                    const uint32_t first = (cb | r | sft) != 0;
 #pragma unroll
-                  for (int k = 0; k < BK / 16; ++k)
-                    mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (cb | t | k) != 0);
-                  if (++sft == a.KW) { sft = 0; ++r; }
+                    for (int k = 0; k < BK / 16; ++k)
+                      mma_bf16(d_base, a0 + off + 2 * k, bd + 2 * k, idesc, k ? 1u : first);
+                    if (MT > 1 && nsub > 1) {
+#pragma unroll
+                      for (int k = 0; k < BK / 16; ++k)
+                        mma_bf16(d_base + BN, a1 + off + 2 * k, bd + 2 * k, idesc, k ? 1u : first);
+                    }
+                  }
                 }
                 mma_commit(&aempty[ast]);
               }
@@ -876,23 +901,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
               continue;
             }
-            int r = 0, sft = 0;
-            for (int t = 0; t < taps; ++t) {
-              if (!g.b_res) {
+            uint32_t roff = 0;
+            for (int r = 0; r < a.KH; ++r, roff += rstep) {
+              for (int sft = 0; sft < a.KW; ++sft) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-              }
-              const uint64_t adesc = make_sdesc_rows(a_base, r * g.we + sft);
-              const uint64_t bdesc = make_sdesc(sB0 + (g.b_res ? (t * g.cblocks + cb) : (int)stage) * C::B_STAGE_BYTES);
-              if (elect_one()) {
+                if (elect_one()) {
+                  const uint64_t bd = make_sdesc(sB0 + (int)stage * C::B_STAGE_BYTES);
+                  const uint32_t off = roff + (uint32_t)sft * 8u;
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k) mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum | k);
-                if (!g.b_res) mma_commit(&empty[stage]);
+                  for (int k = 0; k < BK / 16; ++k) mma_bf16(d_base, a0 + off + 2 * k, bd + 2 * k, idesc, accum | k);
+                  if (MT > 1 && nsub > 1) {
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                      mma_bf16(d_base + BN, a1 + off + 2 * k, bd + 2 * k, idesc, accum | k);
+                  }
+                  mma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                accum = 1;
+                if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
               }
-              __syncwarp();
-              accum = 1;
-              if (!g.b_res && ++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
-              if (++sft == a.KW) { sft = 0; ++r; }
             }
             if (elect_one()) mma_commit(&aempty[ast]);
             __syncwarp();
@@ -966,7 +995,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int blk = 0;
     int iter = 0;
     for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
-      const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+      const int tn = tile - (tile / g.n_tiles) * g.n_tiles;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
       // bias of this tile's columns -> smem (the previous tile's readers are past the
@@ -977,7 +1006,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int sub = 0; sub < MT; ++sub) {
+      const int tm = (tile / g.n_tiles) * MT + sub;
+      if (tm >= g.m_tiles) break;
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (acc * MT + sub) * BN;
       if (!g.tma_out) {
         // final layer straight into the NCHW send buffer (consecutive rows = consecutive
         // pixels, so thread-per-row stores are coalesced per channel)
@@ -1072,6 +1105,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++blk;
         }
       }
+      }  // sub-tiles
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -1082,7 +1116,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS * MT)
                  : "memory");
   }
 }
@@ -1128,7 +1162,8 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   const int res_bytes = g.has_res ? g.res_depth * C::SB_BYTES : 0;
   const int bres_bytes = g.k_chunks * C::B_STAGE_BYTES;
   const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 6 || g.mode == 8;
-  const int a_min = g.mode == 6 ? g.a_stages * g.a_stage_bytes : 4 * A_STAGE_BYTES;
+  const int a_ring = g.a_stages * g.mt * g.a_stage_bytes;  // mode 6 halo ring
+  const int a_min = g.mode == 6 ? a_ring : 4 * A_STAGE_BYTES;
   // resident weights: measured win in halo mode; in modes 3/4 (e.g. the stem) it was slower
   g.b_res = tma_a && g.n_tiles == 1 && (g.mode == 6 || bres_enabled()) &&
             C::FIXED + res_bytes + a_min + bres_bytes <= SMEM_LIMIT;
@@ -1142,13 +1177,13 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   } else if (g.mode == 6) {
     if (g.b_res) {
       g.stages = 1;  // B ring unused
-      smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED + res_bytes;
+      smem = a_ring + bres_bytes + C::FIXED + res_bytes;
     } else {
-      const int rest = SMEM_LIMIT - C::FIXED - res_bytes - g.a_stages * g.a_stage_bytes;
+      const int rest = SMEM_LIMIT - C::FIXED - res_bytes - a_ring;
       g.stages = rest / C::B_STAGE_BYTES;
       if (g.stages > MAX_B_STAGES) g.stages = MAX_B_STAGES;
       if (g.stages < 2) return cudaErrorInvalidValue;
-      smem = g.a_stages * g.a_stage_bytes + g.stages * C::B_STAGE_BYTES + C::FIXED + res_bytes;
+      smem = a_ring + g.stages * C::B_STAGE_BYTES + C::FIXED + res_bytes;
     }
   } else if (g.b_res) {
     g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - bres_bytes) / (g.cps * A_STAGE_BYTES);
@@ -1160,7 +1195,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
     smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes + pro_bytes;
   }
   if (g.stages < 2 && !(g.mode == 6 && g.b_res)) return cudaErrorInvalidValue;
-  const int tiles = g.mode == 8 ? g.n_tasks : g.m_tiles * g.n_tiles;
+  const int tiles = g.mode == 8 ? g.n_tasks : (g.m_tiles + g.mt - 1) / g.mt * g.n_tiles;
   const int grid = tiles < num_sms ? tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
   const CUtensorMap* b = mp.b;
@@ -1175,16 +1210,29 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 2: return launch_t<BN, 2>(a, g, mp, num_sms, st);
     case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
-    case 6: return launch_t<BN, 6>(a, g, mp, num_sms, st);
+    case 6:
+      if (g.mt == 2) {
+        if constexpr (BN <= 128) return launch_t<BN, 9>(a, g, mp, num_sms, st);
+        return cudaErrorInvalidValue;
+      }
+      return launch_t<BN, 6>(a, g, mp, num_sms, st);
     case 7: return launch_t<BN, 7>(a, g, mp, num_sms, st);
     case 8:
-      if (BN == 64) return launch_t<BN, 8>(a, g, mp, num_sms, st);
+      if constexpr (BN == 64) return launch_t<BN, 8>(a, g, mp, num_sms, st);
       return cudaErrorInvalidValue;
   }
   return cudaErrorInvalidValue;
 }
 
 }  // namespace
+
+bool dual_m_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int conv_tc_pick_bn(int cout) {
   if (cout <= 32) return 32;
@@ -1214,6 +1262,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
                            cudaStream_t st) {
   Geo g{};
   g.mode = mode;
+  g.mt = 1;
   g.n_tiles = (a.Cout + bn - 1) / bn;
   g.has_res = a.res != nullptr;
   g.tma_out = !a.nchw;
@@ -1257,6 +1306,15 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     const int rows = rows_read > g.a_bytes / 128 ? rows_read : g.a_bytes / 128;
     g.a_stage_bytes = (rows * 128 + 1023) / 1024 * 1024;
     g.a_stages = 2;
+    // two M sub-tiles per B stage (TMEM: 2 buffers x 2 sub-tiles x BN <= 512 columns): halves
+    // the weight stream from L2 -- measured -25% on ResNet-50 stage-2 3x3 (BN=128); at BN=64
+    // the MMA is smem-bound and it lost 9%, so BN=128 only, and only if >= 4 B stages still fit
+    {
+      const int sb = bn < 64 ? bn : 64;
+      const int fixed = 2 * sb * 2 * BM + bn * 4 + 2048;
+      const int need = 2 * g.a_stages * g.a_stage_bytes + fixed + 4 * bn * BK * 2;
+      if (bn == 128 && g.n_tiles == 1 && !a.res && need <= SMEM_LIMIT && dual_m_enabled()) g.mt = 2;
+    }
   } else if (mode == 4) {
     g.wb = wb; g.hb = hb; g.nb = nb;
     g.tiles_w = (a.OW + wb - 1) / wb;
