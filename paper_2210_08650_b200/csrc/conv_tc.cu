@@ -880,20 +880,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (elect_one()) {
                 uint64_t bd = make_sdesc(sB0 + cb * C::B_STAGE_BYTES);
                 const uint32_t bstep = (uint32_t)(g.cblocks * C::B_STAGE_BYTES) >> 4;
-                uint32_t roff = 0;
-                for (int r = 0; r < a.KH; ++r, roff += rstep) {
-                  for (int sft = 0; sft < a.KW; ++sft, bd += bstep) {
-                    const uint32_t off = roff + (uint32_t)sft * 8u;
-                    const uint32_t first = (cb | r | sft) != 0;
+                const int taps = a.KH * a.KW, kw = a.KW;
+                const uint32_t wrap = rstep - (uint32_t)(kw - 1) * 8u;
+                uint32_t off = 0;
+                int sft = 0;
+                // one flat tap loop (unrolled by the compiler) keeps the MMAs back to back
+#pragma unroll 4
+                for (int t = 0; t < taps; ++t) {
+                  const uint32_t first = (cb | t) != 0;
+#pragma unroll
+                  for (int k = 0; k < BK / 16; ++k)
+                    mma_bf16(d_base, a0 + off + 2 * k, bd + 2 * k, idesc, k ? 1u : first);
+                  if (MT > 1 && nsub > 1) {
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                      mma_bf16(d_base, a0 + off + 2 * k, bd + 2 * k, idesc, k ? 1u : first);
-                    if (MT > 1 && nsub > 1) {
-#pragma unroll
-                      for (int k = 0; k < BK / 16; ++k)
-                        mma_bf16(d_base + BN, a1 + off + 2 * k, bd + 2 * k, idesc, k ? 1u : first);
-                    }
+                      mma_bf16(d_base + BN, a1 + off + 2 * k, bd + 2 * k, idesc, k ? 1u : first);
                   }
+                  bd += bstep;
+                  if (++sft == kw) { sft = 0; off += wrap; } else { off += 8u; }
                 }
                 mma_commit(&aempty[ast]);
               }
@@ -901,14 +905,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
               continue;
             }
-            uint32_t roff = 0;
-            for (int r = 0; r < a.KH; ++r, roff += rstep) {
-              for (int sft = 0; sft < a.KW; ++sft) {
+            {
+              const int taps = a.KH * a.KW, kw = a.KW;
+              const uint32_t wrap = rstep - (uint32_t)(kw - 1) * 8u;
+              uint32_t off = 0;
+              int sft = 0;
+              for (int t = 0; t < taps; ++t) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 if (elect_one()) {
                   const uint64_t bd = make_sdesc(sB0 + (int)stage * C::B_STAGE_BYTES);
-                  const uint32_t off = roff + (uint32_t)sft * 8u;
 #pragma unroll
                   for (int k = 0; k < BK / 16; ++k) mma_bf16(d_base, a0 + off + 2 * k, bd + 2 * k, idesc, accum | k);
                   if (MT > 1 && nsub > 1) {
@@ -921,6 +927,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 __syncwarp();
                 accum = 1;
                 if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+                if (++sft == kw) { sft = 0; off += wrap; } else { off += 8u; }
               }
             }
             if (elect_one()) mma_commit(&aempty[ast]);
@@ -1006,11 +1013,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-#pragma unroll 1
-      for (int sub = 0; sub < MT; ++sub) {
-      const int tm = (tile / g.n_tiles) * MT + sub;
-      if (tm >= g.m_tiles) break;
-      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + (acc * MT + sub) * BN;
+      // one M tile's epilogue (twice per tile in MODE 9)
+      auto epilogue_tile = [&](const int tm, const uint32_t t_row) {
       if (!g.tma_out) {
         // final layer straight into the NCHW send buffer (consecutive rows = consecutive
         // pixels, so thread-per-row stores are coalesced per channel)
@@ -1105,7 +1109,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           ++blk;
         }
       }
-      }  // sub-tiles
+      };
+      const int tm0 = (tile / g.n_tiles) * MT;
+      const uint32_t t_row0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * MT * BN;
+      epilogue_tile(tm0, t_row0);
+      if (MT > 1 && tm0 + 1 < g.m_tiles) epilogue_tile(tm0 + 1, t_row0 + BN);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
