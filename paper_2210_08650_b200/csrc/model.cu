@@ -174,7 +174,9 @@ struct hapi_model {
   void* arena = nullptr;
   int64_t arena_bytes = 0;
   // host pipeline (lazy)
-  cudaStream_t copy_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // host path: H2D copies
+  cudaStream_t out_stream = nullptr;    // host path: D2H copies (separate, so the next H2D never
+                                        // queues behind a D2H that waits for compute)
   void* stage_in[2] = {nullptr, nullptr};
   void* stage_out[2] = {nullptr, nullptr};
   int64_t stage_out_bytes = 0;
@@ -1275,6 +1277,7 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
   for (const Plan& q : m->plans) max_out = std::max(max_out, q.out_bytes_per_img);
   if (!m->host_ready) {
     HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+    HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->out_stream, cudaStreamNonBlocking));
     for (int k = 0; k < 2; ++k) {
       hapi_status st = dev_alloc(m, (size_t)img_bytes * m->d.max_batch, &m->stage_in[k], false);
       if (st == HAPI_OK) st = dev_alloc(m, (size_t)max_out * m->d.max_batch, &m->stage_out[k], false);
@@ -1284,10 +1287,12 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
     m->host_ready = true;
   }
   // ev[0..1] h2d done, ev[2..3] compute done, ev[4..5] d2h done (slot reuse)
-  cudaStream_t cs = m->stream, xs = m->copy_stream;
+  cudaStream_t cs = m->stream, xs = m->copy_stream, ys = m->out_stream;
   // sub-chunks so the H2D copy of chunk i+1 and the D2H of chunk i-1 overlap compute of chunk i
+  // (H2D and D2H on their own streams: PCIe is full duplex)
   uint64_t B = m->d.max_batch;
-  if (batch >= 256) B = std::min<uint64_t>(B, std::max<uint64_t>(64, (batch + 3) / 4));
+  if (const char* e = std::getenv("HAPI_HOST_CHUNK")) B = std::min<uint64_t>(B, std::max(1, std::atoi(e)));
+  else if (batch >= 256) B = std::min<uint64_t>(B, std::max<uint64_t>(64, (batch + 3) / 4));
   const uint64_t nchunks = (batch + B - 1) / B;
   for (uint64_t c = 0; c < nchunks; ++c) {
     const int k = (int)(c & 1);
@@ -1302,12 +1307,13 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
     hapi_status st = run_chunk_graph(m, *p, nb, static_cast<const float*>(m->stage_in[k]), m->stage_out[k]);
     if (st != HAPI_OK) return st;
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[2 + k], cs));
-    HAPI_CUDA_TRY(cudaStreamWaitEvent(xs, m->ev[2 + k], 0));
+    HAPI_CUDA_TRY(cudaStreamWaitEvent(ys, m->ev[2 + k], 0));
     HAPI_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + c0 * p->out_bytes_per_img, m->stage_out[k],
-                                  (size_t)nb * p->out_bytes_per_img, cudaMemcpyDeviceToHost, xs));
-    HAPI_CUDA_TRY(cudaEventRecord(m->ev[4 + k], xs));
+                                  (size_t)nb * p->out_bytes_per_img, cudaMemcpyDeviceToHost, ys));
+    HAPI_CUDA_TRY(cudaEventRecord(m->ev[4 + k], ys));
   }
   HAPI_CUDA_TRY(cudaStreamSynchronize(xs));
+  HAPI_CUDA_TRY(cudaStreamSynchronize(ys));
   HAPI_CUDA_TRY(cudaStreamSynchronize(cs));
   return HAPI_OK;
 }
@@ -1355,8 +1361,10 @@ void hapi_model_destroy(hapi_model* m) {
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
   if (m->host_ready) {
     cudaStreamSynchronize(m->copy_stream);
+    cudaStreamSynchronize(m->out_stream);
     for (auto& e : m->ev) cudaEventDestroy(e);
     cudaStreamDestroy(m->copy_stream);
+    cudaStreamDestroy(m->out_stream);
   }
   for (void* p : m->allocs) cudaFree(p);
   delete m;
