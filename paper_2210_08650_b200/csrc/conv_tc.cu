@@ -340,7 +340,8 @@ template <int BN, int MODE>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const ConvArgs a, const Geo g, const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_y,
-                   const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2) {
+                   const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2,
+                   const __grid_constant__ CUtensorMap tmap_b2) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
   // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
@@ -600,8 +601,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // all weight chunks of the single N tile, once per CTA
       if (elect_one()) {
         mbar_arrive_expect_tx(bres, (uint32_t)g.k_chunks * C::B_STAGE_BYTES);
-        for (int c = 0; c < g.k_chunks; ++c)
-          tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b, c * BK, 0, bres);
+        for (int c = 0; c < g.k_chunks; ++c) {
+          if (a.k2_diag && c >= g.k1_chunks)
+            tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b2, (c - g.k1_chunks) * BK, 0, bres);
+          else
+            tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b, c * BK, 0, bres);
+        }
       }
       __syncwarp();
     }
@@ -689,8 +694,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int ck = kc + j;
                 const uint32_t dA = smem_u32(sA + stage * ASZ + j * A_STAGE_BYTES);
                 if (ck >= g.k1_chunks) {
-                  // fused downsample: 1x1 conv with stride2 over the block input
-                  const int c2 = ck - g.k1_chunks;
+                  // second A source: the fused downsample (1x1/stride2 over the block input), or
+                  // the identity residual (k2_diag) -- channel block tn*BN + 64 j of the residual
+                  // against chunk j of the shared identity (tmap_b2)
+                  const int c2 = ck - g.k1_chunks + (a.k2_diag ? tn * (BN / BK) : 0);
                   if (MODE == 3)
                     tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
                   else
@@ -700,8 +707,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 } else {
                   tma_load_4d(dA, &tmap_a, cb_j * BK, w0 + s_j, h0 + r_j, b0, &full[stage]);
                 }
-                if (!g.b_res)
-                  tma_load_2d(smem_u32(sB + stage * BSZ + j * C::B_STAGE_BYTES), &tmap_b, ck * BK, tn * BN, &full[stage]);
+                if (!g.b_res) {
+                  const uint32_t dB = smem_u32(sB + stage * BSZ + j * C::B_STAGE_BYTES);
+                  if (a.k2_diag && ck >= g.k1_chunks)
+                    tma_load_2d(dB, &tmap_b2, (ck - g.k1_chunks) * BK, 0, &full[stage]);
+                  else
+                    tma_load_2d(dB, &tmap_b, ck * BK, tn * BN, &full[stage]);
+                }
                 if (++cb_j == g.cblocks) {
                   cb_j = 0;
                   if (++s_j == a.KW) { s_j = 0; ++r_j; }
@@ -1208,7 +1220,8 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   if (grid <= 0) return cudaSuccess;
   const CUtensorMap* b = mp.b;
   return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
-                    mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b);
+                    mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b,
+                    mp.b2 ? *mp.b2 : *b);
 }
 
 template <int BN>
@@ -1345,7 +1358,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   }
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {
-    if ((mode != 3 && mode != 4) || !mp.a2) return cudaErrorInvalidValue;
+    if ((mode != 3 && mode != 4) || !mp.a2 || (a.k2_diag && (!mp.b2 || bn > 256))) return cudaErrorInvalidValue;
     g.k_chunks += a.k2_chunks;
   }
   if ((mode == 3 || mode == 4 || mode == 6 || mode == 8) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;

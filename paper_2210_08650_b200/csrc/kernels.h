@@ -71,6 +71,10 @@ struct ConvArgs {
   // stride `stride2` over its own input (TMA modes only)
   int k2_chunks;
   int stride2;
+  // k2_diag = 1: the second source is the identity residual (same rows and channels as the
+  // output) against an identity weight block; each N tile multiplies only its diagonal
+  // BN-channel block (k2_chunks = BN / 64 chunks per tile)
+  int k2_diag;
 };
 
 // tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).  A-operand modes:
@@ -83,6 +87,7 @@ struct ConvArgs {
 struct ConvMaps {
   const CUtensorMap* a;  // A operand (modes 3/4) or nullptr
   const CUtensorMap* a2; // second A source (k2_chunks > 0) or nullptr
+  const CUtensorMap* b2; // k2_diag: the shared 256x256 bf16 identity, box {64, BN}
   const CUtensorMap* b;  // weights
   const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
   const CUtensorMap* r;  // residual view or nullptr

@@ -78,6 +78,14 @@ bool stem_pool_enabled() {
   return on;
 }
 
+bool res_identity_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_RES_GEMM");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool halo_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_HALO");
@@ -108,6 +116,7 @@ struct ConvW {
   int bn = 0, mode = 0;
   double real_flops_per_px = 0;  // 2 * K_real * Cout
   int K2 = 0, cs2 = 0, stride2 = 1;  // fused downsample source (bf16): 1x1/stride2 over cs2 channels
+  bool res_identity = false;         // K2 columns are an identity block: + residual inside the GEMM
 };
 
 enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT };
@@ -170,6 +179,8 @@ struct hapi_model {
   std::vector<const float*> host_params;  // valid during create only
   std::vector<void*> allocs;
   int64_t weight_bytes = 0;
+  void* ident = nullptr;                       // shared 256x256 bf16 identity (residual in GEMM)
+  CUtensorMap ident_map128, ident_map256;      // box {64, 128} / {64, 256}
   std::vector<Plan> plans;  // index split - min_split
   void* arena = nullptr;
   int64_t arena_bytes = 0;
@@ -261,12 +272,15 @@ struct ConvSpec {
   // packed as extra K columns after the first conv's
   std::string w2name, fold2;
   int cin2 = 0, stride2 = 1;
+  // identity residual as the second A source (bf16 1x1): K2 = cout identity columns, so
+  // out = relu(conv(x) + bias + res) comes out of the accumulator (no epilogue residual read)
+  bool res_identity = false;
 };
 
 hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   std::string key = s.wname + "|" + s.bname + "|" + s.fold_bn + "|" + s.pro_bn + "|" + std::to_string(s.cs) + "|" +
                     std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "") + "|" + s.w2name + "|" +
-                    s.fold2;
+                    s.fold2 + (s.res_identity ? "|resid" : "");
   auto it = m->conv_index.find(key);
   if (it != m->conv_index.end()) {
     *out_idx = it->second;
@@ -302,6 +316,14 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   cw.K2 = w2 ? s.cin2 : 0;
   cw.cs2 = s.cin2;
   cw.stride2 = s.stride2;
+  if (s.res_identity) {
+    // the residual joins as a second A source against the model's shared identity block (no
+    // extra weight columns stored)
+    if (!m->bf16 || w2) return set_error(HAPI_ERR_UNSUPPORTED, "identity residual source is a bf16, no-downsample feature");
+    cw.cs2 = s.cout;
+    cw.stride2 = 1;
+    cw.res_identity = true;
+  }
   // element (o, k) of the GEMM B operand, k ordered (r, s, c) over the stored input channels
   auto wval = [&](int o, int r, int t, int c) -> double {
     if (s.s2d) {
@@ -367,6 +389,29 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
       cw.w8 = d8;
     }
     cw.bn = conv_tc_pick_bn(s.cout);
+    if (s.res_identity) {
+      if (cw.bn != 128 && cw.bn != 256) return set_error(HAPI_ERR_UNSUPPORTED, "identity residual needs BN 128/256");
+      if (!m->ident) {
+        std::vector<uint16_t> id(256 * 256, 0);
+        for (int i = 0; i < 256; ++i) id[(size_t)i * 256 + i] = 0x3F80;  // bf16 1.0
+        uint16_t* did;
+        if ((st = upload(m, id, &did)) != HAPI_OK) return st;
+        m->ident = did;
+        EncodeTiledFn enc0 = get_encode_fn();
+        if (!enc0) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        cuuint64_t dims[2] = {256, 256};
+        cuuint64_t strides[1] = {512};
+        cuuint32_t estr[2] = {1, 1};
+        for (int bn2 : {128, 256}) {
+          cuuint32_t box[2] = {64, (cuuint32_t)bn2};
+          CUresult r = enc0(bn2 == 128 ? &m->ident_map128 : &m->ident_map256, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                            m->ident, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+          if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "identity tensor map failed (%d)", (int)r);
+        }
+      }
+    }
     EncodeTiledFn enc = get_encode_fn();
     if (!enc) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)cw.Kp, (cuuint64_t)s.cout};
@@ -490,7 +535,7 @@ struct Builder {
     std::snprintf(d, sizeof(d), "%s %dx%d/s%d C%d->%d %dx%d->%dx%d bn%d mode%d%s%s%s%s%s", cs.wname.c_str(), w.kh,
                   w.kw, w.stride, w.cs, w.cout, in.H, in.W, out.H, out.W, w.bn, o.tc_mode, relu ? " relu" : "",
                   res ? " +res" : "", cs.pro_bn.empty() ? "" : " prologue", cs.s2d ? " s2d" : "",
-                  in2 ? " +fused-downsample" : "");
+                  in2 ? (cs.res_identity ? " +res(in GEMM)" : " +fused-downsample") : "");
     o.desc = d;
     emit(o);
     if (op_out) *op_out = &p.ops.back();
@@ -747,6 +792,15 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           View o = b.compact(md.cout, OH, OW);
           if ((st = b.conv(cl, t, o, true, nullptr, nullptr, &x)) != HAPI_OK) return st;
           cur = o;
+        } else if (md.kind == MK_BOTTLENECK && m->bf16 && md.cout % 64 == 0 && md.planes % 64 == 0 &&
+                   md.planes <= 128 && res_identity_enabled()) {
+          // out = relu(bn(conv(t)) + idn): idn is a second K-concatenated A source against an
+          // identity weight block (diagonal block per N tile), written in place over idn.  The
+          // epilogue-bound small-K convs gain (stage 1: -16%, stage 2: -11%, measured); from
+          // K = 256 the extra BN-deep MMA work cancels the gain (stage 3 equal, stage 4 +21%)
+          cl.res_identity = true;
+          if ((st = b.conv(cl, t, idn, true, nullptr, nullptr, &idn)) != HAPI_OK) return st;
+          cur = idn;
         } else {
           // out = relu(bn(conv(t)) + idn), written in place over idn
           if ((st = b.conv(cl, t, idn, true, &idn)) != HAPI_OK) return st;
@@ -902,8 +956,9 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.relu = o.relu;
       a.nchw = o.nchw_out;
       a.M = (long long)nb * a.OH * a.OW;
-      a.k2_chunks = o.dual ? w.K2 / 64 : 0;
+      a.k2_chunks = o.dual ? (w.res_identity ? w.bn / 64 : w.K2 / 64) : 0;
       a.stride2 = w.stride2;
+      a.k2_diag = w.res_identity ? 1 : 0;
       if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
         a.C = 64; a.KH = 4; a.KW = 1; a.stride = 1; a.pad = 0;
       }
@@ -916,6 +971,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
         ConvMaps mp;
         mp.a = (o.tc_mode >= 3) ? &o.tmap_a : nullptr;
         mp.a2 = o.dual ? &o.tmap_a2 : nullptr;
+        mp.b2 = w.res_identity ? (w.bn == 256 ? &m->ident_map256 : &m->ident_map128) : nullptr;
         mp.b = &w.tmap;
         mp.y = o.nchw_out ? nullptr : &o.tmap_y;
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
