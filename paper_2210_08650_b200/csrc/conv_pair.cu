@@ -1,0 +1,359 @@
+// Chained 1x1 pair on Blackwell tensor cores (sm_100a): a ResNet bottleneck's last conv and
+// the NEXT block's first conv in one persistent kernel.
+//
+// Rows a3/a5 of the hot path: per 128-pixel tile
+//   GEMM1  out = relu(t2 * W3 + bias3 + [x * I | ds(x)])   (conv3 + folded BN + residual,
+//          the residual as a second K-concatenated A source against the identity / the
+//          fused 1x1 downsample weights -- exactly the single-conv path of conv_tc.cu)
+//   GEMM2  t1' = relu(out * W1' + bias1')                  (next block's conv1 + folded BN)
+// The block output tile is written to HBM once (it is the next block's residual) and kept
+// in shared memory as GEMM2's A operand, so conv1' never re-reads it from HBM: that saves
+// the largest activation read of every bottleneck transition (PAPER.md:732 prefix forward;
+// layer-at-a-time it is ~0.9 ms of the ResNet-50 b512 step at HBM peak).
+//
+// Warp roles (10 warps): 0-7 epilogue (thread = TMEM lane; warps w, w+4 split the columns),
+// 8 TMA producer, 9 TMEM allocator + MMA issuer.  TMEM (512 columns): two GEMM1
+// accumulators of BN1 = 128 columns (so the epilogue of N tile j overlaps the MMAs of j+1)
+// and one GEMM2 accumulator of N2 <= 256 columns.  The GEMM1 epilogue writes each 128-column
+// N tile as two 128B-swizzled [128 x 64] bf16 blocks -- the TMA-store staging of `out` and,
+// unchanged, K chunks of GEMM2's A operand (2 N tiles in flight = 4 blocks).
+//
+// Per M tile the MMA order is  G1(0) G1(1) G2(0) G1(2) G2(1) ... G2(last); the producer
+// streams the ring in exactly that order (GEMM1 stages: A + B chunk; GEMM2 stages: B only).
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace hapi {
+namespace {
+using namespace tcx;
+
+constexpr int PM = 128;                  // rows per tile (MMA M)
+constexpr int PK = 64;                   // K chunk (one 128-byte swizzle atom row)
+constexpr int BN1 = 128;                 // GEMM1 N tile
+constexpr int P_EPI_THREADS = 256;
+constexpr int P_PROD_WARP = 8;
+constexpr int P_MMA_WARP = 9;
+constexpr int P_THREADS = 10 * 32;
+constexpr int P_SMEM_LIMIT = 232448;
+constexpr int P_MAX_STAGES = 8;
+constexpr int P_A_BYTES = PM * PK * 2;   // 16 KB
+constexpr int P_STG_BYTES = PM * 64 * 2; // one [128 x 64] bf16 block, 16 KB
+constexpr int P_MAX_BIAS1 = 2048;
+constexpr int P_TMEM_ACC2 = 2 * BN1;     // GEMM2 accumulator column base
+
+template <int N2>
+struct PairCfg {
+  static constexpr int B_BYTES = (N2 > BN1 ? N2 : BN1) * PK * 2;  // GEMM1 (BN1 rows) or GEMM2 (N2 rows) chunk
+  static constexpr int STAGE = P_A_BYTES + B_BYTES;
+  static constexpr int FIXED = 4 * P_STG_BYTES + (P_MAX_BIAS1 + 256) * 4 + 1024 /*barriers*/ + 1024 /*align*/;
+};
+
+__device__ __forceinline__ uint32_t idesc_bf16(int n) {
+  // kind::f16: D fp32, A/B bf16, both K-major, M = 128, N = n
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(PM >> 4) << 24);
+}
+
+template <int N2>
+__global__ void __launch_bounds__(P_THREADS, 1)
+    conv_pair_kernel(const PairArgs a, const int stages, const __grid_constant__ CUtensorMap tm_a1,
+                     const __grid_constant__ CUtensorMap tm_a2, const __grid_constant__ CUtensorMap tm_b1,
+                     const __grid_constant__ CUtensorMap tm_id, const __grid_constant__ CUtensorMap tm_b2,
+                     const __grid_constant__ CUtensorMap tm_y1, const __grid_constant__ CUtensorMap tm_y2) {
+  using C = PairCfg<N2>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;                                  // stages x (A slot | B slot)
+  uint8_t* stg = ring + stages * C::STAGE;               // 4 staging / GEMM2-A blocks
+  float* sBias1 = reinterpret_cast<float*>(stg + 4 * P_STG_BYTES);
+  float* sBias2 = sBias1 + P_MAX_BIAS1;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sBias2 + 256);
+  uint64_t* empty = full + P_MAX_STAGES;
+  uint64_t* tfull1 = empty + P_MAX_STAGES;   // GEMM1 accumulator j&1 ready
+  uint64_t* tempty1 = tfull1 + 2;            // ... drained
+  uint64_t* a2full = tempty1 + 2;            // staging pair j&1 written (GEMM2 may read)
+  uint64_t* a2empty = a2full + 2;            // GEMM2 done reading staging pair j&1
+  uint64_t* tfull2 = a2empty + 2;
+  uint64_t* tempty2 = tfull2 + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty2 + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (int)((a.M + PM - 1) / PM);
+  const int nt1 = a.cout1 / BN1;
+  const int k12 = a.k1_chunks + a.k2_chunks;
+  griddep_launch_dependents();
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull1[i], 1);
+      mbar_init(&tempty1[i], P_EPI_THREADS);
+      mbar_init(&a2full[i], P_EPI_THREADS);
+      mbar_init(&a2empty[i], 1);
+    }
+    mbar_init(tfull2, 1);
+    mbar_init(tempty2, P_EPI_THREADS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == P_PROD_WARP && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_a1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_b2)) : "memory");
+  }
+  if (warp == P_MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  griddep_wait();
+
+  if (warp == P_PROD_WARP) {
+    // ================================================================ TMA producer
+    uint32_t stage = 0, phase = 0;
+    auto next = [&]() {
+      if (++stage == (uint32_t)stages) { stage = 0; phase ^= 1; }
+    };
+    auto load_g1 = [&](int j, int kc, int row0) {
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (elect_one()) {
+        uint64_t* bar = &full[stage];
+        const uint32_t dA = smem_u32(ring + stage * C::STAGE), dB = dA + P_A_BYTES;
+        mbar_arrive_expect_tx(bar, P_A_BYTES + BN1 * PK * 2);
+        if (kc < a.k1_chunks) {
+          tma_load_2d(dA, &tm_a1, kc * PK, row0, bar);
+          tma_load_2d(dB, &tm_b1, kc * PK, j * BN1, bar);
+        } else if (a.k2_diag) {
+          const int c = kc - a.k1_chunks;  // residual channels j*128 + 64c against identity chunk c
+          tma_load_2d(dA, &tm_a2, j * BN1 + c * PK, row0, bar);
+          tma_load_2d(dB, &tm_id, c * PK, 0, bar);
+        } else {
+          const int c = kc - a.k1_chunks;  // fused 1x1 downsample: its weights follow W3's K columns
+          tma_load_2d(dA, &tm_a2, c * PK, row0, bar);
+          tma_load_2d(dB, &tm_b1, kc * PK, j * BN1, bar);
+        }
+      }
+      __syncwarp();
+      next();
+    };
+    auto load_g2 = [&](int jj) {
+      for (int c = 0; c < BN1 / PK; ++c) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (elect_one()) {
+          uint64_t* bar = &full[stage];
+          mbar_arrive_expect_tx(bar, N2 * PK * 2);
+          tma_load_2d(smem_u32(ring + stage * C::STAGE) + P_A_BYTES, &tm_b2, jj * BN1 + c * PK, 0, bar);
+        }
+        __syncwarp();
+        next();
+      }
+    };
+    for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x) {
+      const int row0 = tile * PM;
+      for (int j = 0; j < nt1; ++j) {
+        for (int kc = 0; kc < k12; ++kc) load_g1(j, kc, row0);
+        if (j >= 1) load_g2(j - 1);
+      }
+      load_g2(nt1 - 1);
+    }
+  } else if (warp == P_MMA_WARP) {
+    // ================================================================ MMA issuer
+    const uint32_t id1 = idesc_bf16(BN1), id2 = idesc_bf16(N2);
+    const uint32_t ring0 = smem_u32(ring), stg0 = smem_u32(stg);
+    uint32_t stage = 0, phase = 0;
+    int n = 0, it = 0;
+    auto next = [&]() {
+      if (++stage == (uint32_t)stages) { stage = 0; phase ^= 1; }
+    };
+    auto gemm2 = [&](int nn, bool first_of_tile) {
+      if (first_of_tile) {
+        mbar_wait(tempty2, (it & 1) ^ 1);
+        tc_fence_after();
+      }
+      const int bb = nn & 1;
+      mbar_wait(&a2full[bb], (nn >> 1) & 1);
+      tc_fence_after();
+      for (int c = 0; c < BN1 / PK; ++c) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ad = make_sdesc(stg0 + (bb * 2 + c) * P_STG_BYTES);
+          const uint64_t bd = make_sdesc(ring0 + stage * C::STAGE + P_A_BYTES);
+#pragma unroll
+          for (int k = 0; k < PK / 16; ++k)
+            mma_bf16(tmem + P_TMEM_ACC2, ad + 2 * k, bd + 2 * k, id2, (first_of_tile && c == 0 && k == 0) ? 0u : 1u);
+          mma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        next();
+      }
+      if (elect_one()) mma_commit(&a2empty[bb]);
+      __syncwarp();
+    };
+    for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+      for (int j = 0; j < nt1; ++j, ++n) {
+        const int buf = n & 1;
+        mbar_wait(&tempty1[buf], ((n >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * BN1;
+        for (int kc = 0; kc < k12; ++kc) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ad = make_sdesc(ring0 + stage * C::STAGE);
+            const uint64_t bd = make_sdesc(ring0 + stage * C::STAGE + P_A_BYTES);
+#pragma unroll
+            for (int k = 0; k < PK / 16; ++k) mma_bf16(d, ad + 2 * k, bd + 2 * k, id1, (kc | k) != 0);
+            mma_commit(&empty[stage]);
+          }
+          __syncwarp();
+          next();
+        }
+        if (elect_one()) mma_commit(&tfull1[buf]);
+        __syncwarp();
+        if (j >= 1) gemm2(n - 1, j - 1 == 0);
+      }
+      gemm2(n - 1, nt1 == 1);
+      if (elect_one()) mma_commit(tfull2);
+      __syncwarp();
+    }
+  } else if (warp < 8) {
+    // ================================================================ epilogues
+    const int quarter = warp & 3, gsel = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int et = threadIdx.x;
+    for (int i = et; i < a.cout1; i += P_EPI_THREADS) sBias1[i] = a.bias1 ? __ldg(a.bias1 + i) : 0.f;
+    for (int i = et; i < N2; i += P_EPI_THREADS) sBias2[i] = a.bias2 ? __ldg(a.bias2 + i) : 0.f;
+    epi_bar();
+    const uint32_t stg0 = smem_u32(stg);
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    int n = 0, it = 0;
+    for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
+      const int row0 = tile * PM;
+      for (int j = 0; j < nt1; ++j, ++n) {
+        const int buf = n & 1;
+        mbar_wait(&tfull1[buf], (n >> 1) & 1);
+        tc_fence_after();
+        // staging pair `buf` was last read by GEMM2(n-2) and by the TMA stores of n-2 (and,
+        // for the first N tile of a row tile, by the previous tile's GEMM2-output stores)
+        mbar_wait(&a2empty[buf], ((n >> 1) & 1) ^ 1);
+        if (et == 0) {
+          if (j == 0) bulk_wait_read0(); else bulk_wait_read1();
+        }
+        epi_bar();
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          uint32_t v[32];
+          tmem_ld32(lane_base + buf * BN1 + b * 64 + gsel * 32, v);
+          tmem_wait_ld();
+          const uint32_t blk = stg0 + (buf * 2 + b) * P_STG_BYTES;
+          const float* bias = sBias1 + j * BN1 + b * 64 + gsel * 32;
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              o[q] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * q]) + bias[c4 * 8 + 2 * q],
+                                     __uint_as_float(v[c4 * 8 + 2 * q + 1]) + bias[c4 * 8 + 2 * q + 1]);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk + swz_off<128>(row, gsel * 4 + c4)),
+                         "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                         : "memory");
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty1[buf]);
+        fence_proxy_async_smem();
+        mbar_arrive(&a2full[buf]);
+        epi_bar();
+        if (et == 0) {
+          for (int b = 0; b < 2; ++b)
+            tma_store_2d(&tm_y1, stg0 + (buf * 2 + b) * P_STG_BYTES, j * BN1 + b * 64, row0);
+          bulk_commit();
+        }
+      }
+      // GEMM2 epilogue: t1' = relu(acc2 + bias2) through staging blocks 0..N2/64-1 (every
+      // GEMM2 of this tile has completed -- tfull2 -- so only the store reads are pending)
+      mbar_wait(tfull2, it & 1);
+      tc_fence_after();
+      if (et == 0) bulk_wait_read0();
+      epi_bar();
+#pragma unroll
+      for (int b = 0; b < N2 / 64; ++b) {
+        uint32_t v[32];
+        tmem_ld32(lane_base + P_TMEM_ACC2 + b * 64 + gsel * 32, v);
+        tmem_wait_ld();
+        const uint32_t blk = stg0 + b * P_STG_BYTES;
+        const float* bias = sBias2 + b * 64 + gsel * 32;
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          uint32_t o[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            o[q] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * q]) + bias[c4 * 8 + 2 * q],
+                                   __uint_as_float(v[c4 * 8 + 2 * q + 1]) + bias[c4 * 8 + 2 * q + 1]);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk + swz_off<128>(row, gsel * 4 + c4)),
+                       "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                       : "memory");
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty2);
+      fence_proxy_async_smem();
+      epi_bar();
+      if (et == 0) {
+        for (int b = 0; b < N2 / 64; ++b) tma_store_2d(&tm_y2, stg0 + b * P_STG_BYTES, b * 64, row0);
+        bulk_commit();
+      }
+    }
+    if (et == 0) bulk_wait_all();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == P_MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int N2>
+cudaError_t launch_pair(const PairArgs& a, const PairMaps& mp, int num_sms, cudaStream_t st) {
+  using C = PairCfg<N2>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(conv_pair_kernel<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_LIMIT);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int stages = (P_SMEM_LIMIT - C::FIXED) / C::STAGE;
+  if (stages > P_MAX_STAGES) stages = P_MAX_STAGES;
+  if (stages < 2) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)stages * C::STAGE + C::FIXED;
+  const long long m_tiles = (a.M + PM - 1) / PM;
+  const int grid = (int)(m_tiles < num_sms ? m_tiles : num_sms);
+  if (grid <= 0) return cudaSuccess;
+  return launch_pdl(conv_pair_kernel<N2>, dim3(grid), dim3(P_THREADS), smem, st, a, stages, *mp.a1, *mp.a2, *mp.b1,
+                    *mp.id, *mp.b2, *mp.y1, *mp.y2);
+}
+
+}  // namespace
+
+cudaError_t conv_pair_launch(const PairArgs& a, const PairMaps& mp, int n2, int num_sms, cudaStream_t st) {
+  if (a.cout1 % BN1 != 0 || a.cout1 > P_MAX_BIAS1 || a.k1_chunks < 1 || a.k2_chunks < 0 ||
+      (a.k2_diag && a.k2_chunks != BN1 / PK) || !mp.a1 || !mp.b1 || !mp.b2 || !mp.y1 || !mp.y2 ||
+      (a.k2_chunks > 0 && !mp.a2) || (a.k2_diag && !mp.id))
+    return cudaErrorInvalidValue;
+  switch (n2) {
+    case 64: return launch_pair<64>(a, mp, num_sms, st);
+    case 128: return launch_pair<128>(a, mp, num_sms, st);
+    case 256: return launch_pair<256>(a, mp, num_sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace hapi

@@ -92,6 +92,28 @@ struct ConvMaps {
   const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
   const CUtensorMap* r;  // residual view or nullptr
 };
+// Chained 1x1 pair (conv_pair.cu): a bottleneck's conv3 (+ residual as second A source) and
+// the next block's conv1 per 128-row tile; the block output tile stays in smem as conv1's A.
+struct PairArgs {
+  long long M;          // rows (pixels) of both GEMMs
+  int k1_chunks;        // conv3 K / 64 (A from a1, B from b1 columns)
+  int k2_chunks;        // second A source chunks per 128-wide N tile: diag = 2, fused ds = its K / 64
+  int k2_diag;          // 1: identity residual (a2 channel block of the N tile x identity b2-id)
+  int cout1;            // conv3 output channels (multiple of 128, <= 2048)
+  const float* bias1;   // [cout1] conv3 bias (+ ds bias)
+  const float* bias2;   // [n2] next conv1 bias
+};
+struct PairMaps {
+  const CUtensorMap* a1;  // t2 [M][K1], box {64, 128}
+  const CUtensorMap* a2;  // residual / ds input [M][C2], box {64, 128}
+  const CUtensorMap* b1;  // conv3 weights [cout1][Kp], box {64, 128}
+  const CUtensorMap* id;  // 256x256 identity, box {64, 128}
+  const CUtensorMap* b2;  // next conv1 weights [n2][cout1], box {64, n2}
+  const CUtensorMap* y1;  // block output view [M][cout1], box {64, 128}, 128B swizzle
+  const CUtensorMap* y2;  // next conv1 output view [M][n2], box {64, 128}, 128B swizzle
+};
+cudaError_t conv_pair_launch(const PairArgs& a, const PairMaps& mp, int n2, int num_sms, cudaStream_t st);
+
 int conv_tc_pick_bn(int cout);
 int conv_tc_store_cols(int bn);  // columns per epilogue TMA box (64, or bn if smaller)
 void conv_tc_spatial_tile(int OH, int OW, int N, int* wb, int* hb, int* nb);

@@ -78,6 +78,14 @@ bool stem_pool_enabled() {
   return on;
 }
 
+bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool res_identity_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_RES_GEMM");
@@ -119,7 +127,7 @@ struct ConvW {
   bool res_identity = false;         // K2 columns are an identity block: + residual inside the GEMM
 };
 
-enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT };
+enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT, OP_PAIR };
 
 struct View {
   int buf = -1;       // -1: external (caller out, or caller images for PACK_IN input)
@@ -148,6 +156,12 @@ struct Op {
   bool dual = false;             // second A source (fused downsample) = in2
   View in2;
   CUtensorMap tmap_a2;
+  // OP_PAIR (conv_pair.cu): conv = the bottleneck's conv3, conv2 = the next block's conv1,
+  // out = block output, out2 = next conv1 output
+  int conv2 = -1;
+  View out2;
+  CUtensorMap tmap_b1;           // conv3 weights with a {64, 128} box
+  CUtensorMap tmap_y2;
 };
 
 struct Buf {
@@ -851,6 +865,38 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     }
   }
 
+  // Peephole: a bottleneck's last conv (1x1, residual or stride-1 downsample as second A
+  // source) directly followed by the next block's 1x1 conv1 reading its output becomes one
+  // OP_PAIR launch -- the block output tile stays in smem as conv1's A operand.
+  if (m->bf16 && pair_enabled()) {
+    std::vector<Op>& ops = b.p.ops;
+    for (size_t k = 0; k + 1 < ops.size(); ++k) {
+      Op& A = ops[k];
+      const Op& B = ops[k + 1];
+      if (A.t != OP_CONV || B.t != OP_CONV || A.tc_mode != 3 || !A.dual || A.has_res || !A.relu || A.nchw_out) continue;
+      if (B.tc_mode != 3 || B.dual || B.has_res || !B.relu || B.nchw_out) continue;
+      const ConvW& wa = m->convs[A.conv];
+      const ConvW& wb = m->convs[B.conv];
+      const bool ds1 = !wa.res_identity && wa.stride2 == 1 && wa.K2 % 64 == 0 && wa.K2 > 0;
+      if (!(wa.res_identity || ds1) || wa.kh != 1 || wa.K % 64 != 0 || wa.cout % 128 != 0 || wa.cout > 2048) continue;
+      if (wb.kh != 1 || wb.stride != 1 || wb.pro_scale || wb.cs != wa.cout || wb.bn != wb.cout ||
+          (wb.cout != 64 && wb.cout != 128 && wb.cout != 256))
+        continue;
+      if (B.in.buf != A.out.buf || B.in.coff != A.out.coff || B.in.ld != A.out.ld || A.out.buf < 0 || B.out.buf < 0 ||
+          A.out.ld != A.out.C || B.out.ld != B.out.C)
+        continue;
+      Op P = A;
+      P.t = OP_PAIR;
+      P.conv2 = B.conv;
+      P.out2 = B.out;
+      P.flops = A.flops + B.flops;
+      P.bytes = A.bytes + (double)B.out.H * B.out.W * B.out.C * m->es;
+      P.desc = "pair[" + A.desc + " => " + B.desc + "]";
+      ops[k] = P;
+      ops.erase(ops.begin() + (long)k + 1);
+    }
+  }
+
   // a7: deliver layer `split` into the caller's buffer as contiguous NCHW.
   Plan& p = b.p;
   b.p.out_bytes_per_img = (int64_t)cur.C * cur.H * cur.W * m->es;
@@ -886,6 +932,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     if (o.has_res) touch(o.res.buf);
     if (o.dual) touch(o.in2.buf);
     touch(o.out.buf);
+    if (o.t == OP_PAIR) touch(o.out2.buf);
   }
   const int64_t B = m->d.max_batch;
   std::vector<int> order;
@@ -936,6 +983,28 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
     case OP_PACK_IN:
       e = pack_input_launch(images, vptr(m, p, o.out, out), nb, (int)m->d.in_h, (int)m->d.in_w, o.layout, st);
       break;
+    case OP_PAIR: {
+      const ConvW& wa = m->convs[o.conv];
+      const ConvW& wb = m->convs[o.conv2];
+      PairArgs a;
+      a.M = (long long)nb * o.out.H * o.out.W;
+      a.k1_chunks = wa.K / 64;
+      a.k2_diag = wa.res_identity ? 1 : 0;
+      a.k2_chunks = wa.res_identity ? 2 : wa.K2 / 64;
+      a.cout1 = wa.cout;
+      a.bias1 = wa.bias;
+      a.bias2 = wb.bias;
+      PairMaps mp;
+      mp.a1 = &o.tmap_a;
+      mp.a2 = &o.tmap_a2;
+      mp.b1 = &o.tmap_b1;
+      mp.id = &m->ident_map128;
+      mp.b2 = &wb.tmap;
+      mp.y1 = &o.tmap_y;
+      mp.y2 = &o.tmap_y2;
+      e = conv_pair_launch(a, mp, wb.cout, m->num_sms, st);
+      break;
+    }
     case OP_CONV: {
       const ConvW& w = m->convs[o.conv];
       ConvArgs a;
@@ -1075,9 +1144,23 @@ hapi_status finalize_tmaps(hapi_model* m) {
   if (!m->bf16) return HAPI_OK;
   for (Plan& p : m->plans) {
     for (Op& o : p.ops) {
-      if (o.t != OP_CONV) continue;
+      if (o.t != OP_CONV && o.t != OP_PAIR) continue;
       const ConvW& w = m->convs[o.conv];
       hapi_status st = HAPI_OK;
+      if (o.t == OP_PAIR) {
+        // conv3 weights with the pair kernel's 128-row N tile, and the next conv1's output view
+        EncodeTiledFn enc = get_encode_fn();
+        if (!enc) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        cuuint64_t dims[2] = {(cuuint64_t)w.Kp, (cuuint64_t)w.cout};
+        cuuint64_t strides[1] = {(cuuint64_t)w.Kp * 2};
+        cuuint32_t box[2] = {64, 128};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = enc(&o.tmap_b1, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w.w, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "pair weight tensor map failed (%d)", (int)r);
+        if ((st = encode_view(m, p, o, o.out2, 64, &o.tmap_y2, "Y2")) != HAPI_OK) return st;
+      }
       if (o.tc_mode == 8) {
         // halo box over the padded s2d input [N][HP][WP][16]: {8 channels, wb + 3, 2 + 3, 1},
         // loaded twice (channels 0-7, 8-15) into two 16-byte-per-pixel planes
@@ -1388,7 +1471,7 @@ hapi_status hapi_plan_describe(const hapi_model* m, uint32_t split_idx, uint32_t
   if (split_idx < m->d.min_split || split_idx > m->d.max_split) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx");
   const Plan& p = m->plans[split_idx - m->d.min_split];
   if (op >= p.ops.size()) return set_error(HAPI_ERR_INVALID_ARGUMENT, "op index");
-  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out"};
+  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out", "pair"};
   const Op& o = p.ops[op];
   std::snprintf(buf, cap, "%s%s%s", o.desc.empty() ? names[o.t] : o.desc.c_str(), o.out.buf < 0 ? " ->out" : "",
                 o.nchw_out ? "(nchw)" : "");
