@@ -11,15 +11,18 @@
 // the largest activation read of every bottleneck transition (PAPER.md:732 prefix forward;
 // layer-at-a-time it is ~0.9 ms of the ResNet-50 b512 step at HBM peak).
 //
-// Warp roles (10 warps): 0-7 epilogue (thread = TMEM lane; warps w, w+4 split the columns),
-// 8 TMA producer, 9 TMEM allocator + MMA issuer.  TMEM (512 columns): two GEMM1
+// Warp roles (11 warps): 0-7 epilogue (thread = TMEM lane; warps w, w+4 split the columns),
+// 8 TMA producer of GEMM1 (A + W3 chunks), 9 TMEM allocator + MMA issuer, 10 TMA producer of
+// GEMM2's weight chunks (own ring: GEMM2 stages wait on the epilogue, and must not block
+// the next tile's GEMM1 prefetch).  (Keeping t2 and the identity block resident in smem
+// instead was measured slower: it leaves fewer bytes in flight for the HBM streams.)  TMEM (512 columns): two GEMM1
 // accumulators of BN1 = 128 columns (so the epilogue of N tile j overlaps the MMAs of j+1)
 // and one GEMM2 accumulator of N2 <= 256 columns.  The GEMM1 epilogue writes each 128-column
 // N tile as two 128B-swizzled [128 x 64] bf16 blocks -- the TMA-store staging of `out` and,
 // unchanged, K chunks of GEMM2's A operand (2 N tiles in flight = 4 blocks).
 //
-// Per M tile the MMA order is  G1(0) G1(1) G2(0) G1(2) G2(1) ... G2(last); the producer
-// streams the ring in exactly that order (GEMM1 stages: A + B chunk; GEMM2 stages: B only).
+// Per M tile the MMA order is  G1(0) G1(1) G2(0) G1(2) G2(1) ... G2(last); each producer
+// streams its ring in that order.
 #include "kernels.h"
 #include "tc_ptx.cuh"
 
@@ -33,19 +36,22 @@ constexpr int BN1 = 128;                 // GEMM1 N tile
 constexpr int P_EPI_THREADS = 256;
 constexpr int P_PROD_WARP = 8;
 constexpr int P_MMA_WARP = 9;
-constexpr int P_THREADS = 10 * 32;
+constexpr int P_PROD2_WARP = 10;
+constexpr int P_THREADS = 11 * 32;
+constexpr int P_S2 = 2;                  // GEMM2 weight ring depth
 constexpr int P_SMEM_LIMIT = 232448;
 constexpr int P_MAX_STAGES = 8;
 constexpr int P_A_BYTES = PM * PK * 2;   // 16 KB
 constexpr int P_STG_BYTES = PM * 64 * 2; // one [128 x 64] bf16 block, 16 KB
-constexpr int P_MAX_BIAS1 = 2048;
+constexpr int P_MAX_BIAS1 = 512;
 constexpr int P_TMEM_ACC2 = 2 * BN1;     // GEMM2 accumulator column base
 
 template <int N2>
 struct PairCfg {
-  static constexpr int B_BYTES = (N2 > BN1 ? N2 : BN1) * PK * 2;  // GEMM1 (BN1 rows) or GEMM2 (N2 rows) chunk
-  static constexpr int STAGE = P_A_BYTES + B_BYTES;
-  static constexpr int FIXED = 4 * P_STG_BYTES + (P_MAX_BIAS1 + 256) * 4 + 1024 /*barriers*/ + 1024 /*align*/;
+  static constexpr int STAGE = P_A_BYTES + BN1 * PK * 2;  // GEMM1 ring: A chunk + W3 chunk
+  static constexpr int B2_BYTES = N2 * PK * 2;            // GEMM2 ring: one W1' chunk
+  static constexpr int FIXED = 4 * P_STG_BYTES + P_S2 * B2_BYTES + (P_MAX_BIAS1 + 256) * 4 + 1024 /*barriers*/ +
+                               1024 /*align*/;
 };
 
 __device__ __forceinline__ uint32_t idesc_bf16(int n) {
@@ -64,7 +70,8 @@ __global__ void __launch_bounds__(P_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;                                  // stages x (A slot | B slot)
   uint8_t* stg = ring + stages * C::STAGE;               // 4 staging / GEMM2-A blocks
-  float* sBias1 = reinterpret_cast<float*>(stg + 4 * P_STG_BYTES);
+  uint8_t* ring2 = stg + 4 * P_STG_BYTES;                // GEMM2 weight chunks
+  float* sBias1 = reinterpret_cast<float*>(ring2 + P_S2 * C::B2_BYTES);
   float* sBias2 = sBias1 + P_MAX_BIAS1;
   uint64_t* full = reinterpret_cast<uint64_t*>(sBias2 + 256);
   uint64_t* empty = full + P_MAX_STAGES;
@@ -74,7 +81,9 @@ __global__ void __launch_bounds__(P_THREADS, 1)
   uint64_t* a2empty = a2full + 2;            // GEMM2 done reading staging pair j&1
   uint64_t* tfull2 = a2empty + 2;
   uint64_t* tempty2 = tfull2 + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty2 + 1);
+  uint64_t* full2 = tempty2 + 1;
+  uint64_t* empty2 = full2 + P_S2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty2 + P_S2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m_tiles = (int)((a.M + PM - 1) / PM);
@@ -95,6 +104,10 @@ __global__ void __launch_bounds__(P_THREADS, 1)
     }
     mbar_init(tfull2, 1);
     mbar_init(tempty2, P_EPI_THREADS);
+    for (int i = 0; i < P_S2; ++i) {
+      mbar_init(&full2[i], 1);
+      mbar_init(&empty2[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == P_PROD_WARP && lane == 0) {
@@ -141,31 +154,32 @@ __global__ void __launch_bounds__(P_THREADS, 1)
       __syncwarp();
       next();
     };
-    auto load_g2 = [&](int jj) {
-      for (int c = 0; c < BN1 / PK; ++c) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (elect_one()) {
-          uint64_t* bar = &full[stage];
-          mbar_arrive_expect_tx(bar, N2 * PK * 2);
-          tma_load_2d(smem_u32(ring + stage * C::STAGE) + P_A_BYTES, &tm_b2, jj * BN1 + c * PK, 0, bar);
-        }
-        __syncwarp();
-        next();
-      }
-    };
     for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x) {
       const int row0 = tile * PM;
-      for (int j = 0; j < nt1; ++j) {
+      for (int j = 0; j < nt1; ++j)
         for (int kc = 0; kc < k12; ++kc) load_g1(j, kc, row0);
-        if (j >= 1) load_g2(j - 1);
+    }
+  } else if (warp == P_PROD2_WARP) {
+    // ================================================================ GEMM2 weight producer
+    uint32_t stage = 0, phase = 0;
+    for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x) {
+      for (int jj = 0; jj < nt1; ++jj) {
+        for (int c = 0; c < BN1 / PK; ++c) {
+          mbar_wait(&empty2[stage], phase ^ 1);
+          if (elect_one()) {
+            mbar_arrive_expect_tx(&full2[stage], C::B2_BYTES);
+            tma_load_2d(smem_u32(ring2 + stage * C::B2_BYTES), &tm_b2, jj * BN1 + c * PK, 0, &full2[stage]);
+          }
+          __syncwarp();
+          if (++stage == (uint32_t)P_S2) { stage = 0; phase ^= 1; }
+        }
       }
-      load_g2(nt1 - 1);
     }
   } else if (warp == P_MMA_WARP) {
     // ================================================================ MMA issuer
     const uint32_t id1 = idesc_bf16(BN1), id2 = idesc_bf16(N2);
-    const uint32_t ring0 = smem_u32(ring), stg0 = smem_u32(stg);
-    uint32_t stage = 0, phase = 0;
+    const uint32_t ring0 = smem_u32(ring), stg0 = smem_u32(stg), ring20 = smem_u32(ring2);
+    uint32_t stage = 0, phase = 0, stage2 = 0, phase2 = 0;
     int n = 0, it = 0;
     auto next = [&]() {
       if (++stage == (uint32_t)stages) { stage = 0; phase ^= 1; }
@@ -179,18 +193,18 @@ __global__ void __launch_bounds__(P_THREADS, 1)
       mbar_wait(&a2full[bb], (nn >> 1) & 1);
       tc_fence_after();
       for (int c = 0; c < BN1 / PK; ++c) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait(&full2[stage2], phase2);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t ad = make_sdesc(stg0 + (bb * 2 + c) * P_STG_BYTES);
-          const uint64_t bd = make_sdesc(ring0 + stage * C::STAGE + P_A_BYTES);
+          const uint64_t bd = make_sdesc(ring20 + stage2 * C::B2_BYTES);
 #pragma unroll
           for (int k = 0; k < PK / 16; ++k)
             mma_bf16(tmem + P_TMEM_ACC2, ad + 2 * k, bd + 2 * k, id2, (first_of_tile && c == 0 && k == 0) ? 0u : 1u);
-          mma_commit(&empty[stage]);
+          mma_commit(&empty2[stage2]);
         }
         __syncwarp();
-        next();
+        if (++stage2 == (uint32_t)P_S2) { stage2 = 0; phase2 ^= 1; }
       }
       if (elect_one()) mma_commit(&a2empty[bb]);
       __syncwarp();
@@ -252,14 +266,16 @@ __global__ void __launch_bounds__(P_THREADS, 1)
           tmem_ld32(lane_base + buf * BN1 + b * 64 + gsel * 32, v);
           tmem_wait_ld();
           const uint32_t blk = stg0 + (buf * 2 + b) * P_STG_BYTES;
-          const float* bias = sBias1 + j * BN1 + b * 64 + gsel * 32;
+          const uint32_t bias = smem_u32(sBias1 + j * BN1 + b * 64 + gsel * 32);
 #pragma unroll
           for (int c4 = 0; c4 < 4; ++c4) {
+            const float4 b0 = lds_f4(bias + c4 * 32), b1 = lds_f4(bias + c4 * 32 + 16);
+            const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
             uint32_t o[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              o[q] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * q]) + bias[c4 * 8 + 2 * q],
-                                     __uint_as_float(v[c4 * 8 + 2 * q + 1]) + bias[c4 * 8 + 2 * q + 1]);
+              o[q] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * q]) + bb[2 * q],
+                                     __uint_as_float(v[c4 * 8 + 2 * q + 1]) + bb[2 * q + 1]);
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk + swz_off<128>(row, gsel * 4 + c4)),
                          "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
                          : "memory");
@@ -288,14 +304,16 @@ __global__ void __launch_bounds__(P_THREADS, 1)
         tmem_ld32(lane_base + P_TMEM_ACC2 + b * 64 + gsel * 32, v);
         tmem_wait_ld();
         const uint32_t blk = stg0 + b * P_STG_BYTES;
-        const float* bias = sBias2 + b * 64 + gsel * 32;
+        const uint32_t bias = smem_u32(sBias2 + b * 64 + gsel * 32);
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
+          const float4 b0 = lds_f4(bias + c4 * 32), b1 = lds_f4(bias + c4 * 32 + 16);
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
           uint32_t o[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            o[q] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * q]) + bias[c4 * 8 + 2 * q],
-                                   __uint_as_float(v[c4 * 8 + 2 * q + 1]) + bias[c4 * 8 + 2 * q + 1]);
+            o[q] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * q]) + bb[2 * q],
+                                   __uint_as_float(v[c4 * 8 + 2 * q + 1]) + bb[2 * q + 1]);
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk + swz_off<128>(row, gsel * 4 + c4)),
                        "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
@@ -351,7 +369,6 @@ cudaError_t conv_pair_launch(const PairArgs& a, const PairMaps& mp, int n2, int 
   switch (n2) {
     case 64: return launch_pair<64>(a, mp, num_sms, st);
     case 128: return launch_pair<128>(a, mp, num_sms, st);
-    case 256: return launch_pair<256>(a, mp, num_sms, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -880,7 +880,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
       const bool ds1 = !wa.res_identity && wa.stride2 == 1 && wa.K2 % 64 == 0 && wa.K2 > 0;
       if (!(wa.res_identity || ds1) || wa.kh != 1 || wa.K % 64 != 0 || wa.cout % 128 != 0 || wa.cout > 2048) continue;
       if (wb.kh != 1 || wb.stride != 1 || wb.pro_scale || wb.cs != wa.cout || wb.bn != wb.cout ||
-          (wb.cout != 64 && wb.cout != 128 && wb.cout != 256))
+          (wb.cout != 64 && wb.cout != 128) || wa.K > 128 || wa.cout > 512)
         continue;
       if (B.in.buf != A.out.buf || B.in.coff != A.out.coff || B.in.ld != A.out.ld || A.out.buf < 0 || B.out.buf < 0 ||
           A.out.ld != A.out.C || B.out.ld != B.out.C)

@@ -1,0 +1,56 @@
+"""Fusions that must not change a single output bit (GPU).
+
+The chained conv3 -> next-conv1 pair kernel (conv_pair.cu) keeps the block output tile in
+shared memory instead of re-reading it, but every GEMM sees the same bf16 operands in the same
+K order as the unfused launches, so the split-layer output must be bitwise identical with the
+peephole switched off (HAPI_PAIR=0).  The same holds for the resident-weight / dual-M halo
+variants and the stem+maxpool fusion (relu and max commute with the bf16 rounding).  Each
+variant runs in its own process because the switches are read once per process.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import hapi_inputs
+from tests.gpu_helpers import gpu_forward
+arch, split, size, n, out = {arch!r}, {split}, {size}, {n}, {out!r}
+P = hapi_inputs.params(arch, 11)
+x = hapi_inputs.images(n, 12, size, size)
+y, m = gpu_forward(arch, "bf16", split, x, P)
+m.close()
+np.save(out, y)
+"""
+
+
+def _run(tmp_path, env_extra, arch, split, size, n, tag):
+    out = str(tmp_path / f"{tag}.npy")
+    env = dict(os.environ)
+    env.update(env_extra)
+    code = _SNIPPET.format(root=ROOT, arch=arch, split=split, size=size, n=n, out=out)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(out)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("arch,split,size,n,flag", [
+    ("resnet50", 21, 96, 6, "HAPI_PAIR"),        # pair kernel (stage 1 ds/identity pairs, stage 2 pairs)
+    ("resnet50", 9, 64, 5, "HAPI_PAIR"),         # split right after a paired block boundary
+    ("resnet50", 21, 96, 6, "HAPI_STEM_POOL"),   # stem conv + maxpool fusion
+    ("densenet121", 9, 64, 5, "HAPI_STEM_POOL"),
+    ("resnet50", 21, 96, 6, "HAPI_DUAL_M"),      # two M sub-tiles per weight stage (halo mode)
+])
+def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag):
+    fused = _run(tmp_path, {}, arch, split, size, n, "on")
+    plain = _run(tmp_path, {flag: "0"}, arch, split, size, n, "off")
+    assert fused.shape == plain.shape
+    assert np.array_equal(fused.view(np.uint32), plain.view(np.uint32)), (
+        flag, int((fused != plain).sum()), float(np.abs(fused - plain).max()))
