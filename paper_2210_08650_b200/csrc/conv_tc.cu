@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
   constexpr bool HALO = (MODE == 6 || MODE == 9);
   constexpr int MT = MODE == 9 ? 2 : 1;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || HALO || MODE == 7 || MODE == 8);
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 5 || HALO || MODE == 7 || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   const int S = g.stages;
   const int AS = (HALO || MODE == 8) ? g.a_stages : S;
@@ -507,6 +507,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tile_origin(g, tm, &ow0, &oh0, &b0);
             w0 = ow0 * a.stride - a.pad;
             h0 = oh0 * a.stride - a.pad;
+          } else if (MODE == 5) {
+            // flat tile: its first output pixel (n, oh, ow) -> im2col start position
+            const long long m0 = (long long)tm * BM;
+            b0 = (int)(m0 / OHW);
+            const int rem = (int)(m0 - (long long)b0 * OHW);
+            oh0 = rem / a.OW;
+            ow0 = rem - oh0 * a.OW;
+            w0 = ow0 * a.stride - a.pad;
+            h0 = oh0 * a.stride - a.pad;
           }
           int cb = 0, r = 0, sft = 0;  // (tap, channel block) of chunk kc, tracked incrementally
           for (int kc = 0; kc < g.k_chunks; kc += CPS) {
@@ -525,10 +534,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   const int c2 = ck - g.k1_chunks + (a.k2_diag ? tn * (BN / BK) : 0);
                   if (MODE == 3)
                     tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
+                  else if (MODE == 5)
+                    tma_load_im2col_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, 0, 0, &full[stage]);
                   else
                     tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
                 } else if (MODE == 3) {
                   tma_load_2d(dA, &tmap_a, ck * BK, tm * BM, &full[stage]);
+                } else if (MODE == 5) {
+                  tma_load_im2col_4d(dA, &tmap_a, cb_j * BK, w0, h0, b0, (uint16_t)s_j, (uint16_t)r_j, &full[stage]);
                 } else {
                   tma_load_4d(dA, &tmap_a, cb_j * BK, w0 + s_j, h0 + r_j, b0, &full[stage]);
                 }
@@ -1006,7 +1019,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   g.res_depth = res_depth_pick(g.cps * C::STAGE_BYTES, C::FIXED, C::SB_BYTES);
   const int res_bytes = g.has_res ? g.res_depth * C::SB_BYTES : 0;
   const int bres_bytes = g.k_chunks * C::B_STAGE_BYTES;
-  const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 6 || g.mode == 8;
+  const bool tma_a = g.mode == 3 || g.mode == 4 || g.mode == 5 || g.mode == 6 || g.mode == 8;
   const int a_ring = g.a_stages * g.mt * g.a_stage_bytes;  // mode 6 halo ring
   const int a_min = g.mode == 6 ? a_ring : 4 * A_STAGE_BYTES;
   // resident weights: measured win in halo mode; in modes 3/4 (e.g. the stem) it was slower
@@ -1056,6 +1069,7 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 2: return launch_t<BN, 2>(a, g, mp, num_sms, st);
     case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
+    case 5: return launch_t<BN, 5>(a, g, mp, num_sms, st);
     case 6:
       if (g.mt == 2) {
         if constexpr (BN <= 128) return launch_t<BN, 9>(a, g, mp, num_sms, st);
@@ -1183,10 +1197,10 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   }
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {
-    if ((mode != 3 && mode != 4) || !mp.a2 || (a.k2_diag && (!mp.b2 || bn > 256))) return cudaErrorInvalidValue;
+    if ((mode != 3 && mode != 4 && mode != 5) || !mp.a2 || (a.k2_diag && (!mp.b2 || bn > 256))) return cudaErrorInvalidValue;
     g.k_chunks += a.k2_chunks;
   }
-  if ((mode == 3 || mode == 4 || mode == 6 || mode == 8) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
+  if ((mode == 3 || mode == 4 || mode == 5 || mode == 6 || mode == 8) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
   if (g.tma_out && !mp.y) return cudaErrorInvalidValue;
   if (g.has_res && g.tma_out && !mp.r) return cudaErrorInvalidValue;
   if (g.has_res && !g.tma_out) g.has_res = 0;  // NCHW path reads the residual directly

@@ -50,6 +50,31 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn get_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  }
+  return fn;
+}
+
+bool im2col_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_IM2COL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 EncodeTiledFn get_encode_fn() {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
@@ -511,6 +536,8 @@ struct Builder {
         // fused downsample: both A sources must produce rows in the same order
         if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0 && cs.stride2 == 1) {
           o.tc_mode = 3;
+        } else if (im2col_enabled()) {
+          o.tc_mode = 5;  // flat 128-row tiles, both sources through im2col TMA
         } else {
           conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
           o.tc_mode = 4;
@@ -535,6 +562,8 @@ struct Builder {
           o.wb = out.W;
           o.nb = 1;
           o.tc_mode = 6;
+        } else if (im2col_enabled()) {
+          o.tc_mode = 5;  // strided / small maps: im2col TMA per tap, full 128-row tiles
         } else if (w.stride <= 2) {
           conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
           if (o.wb * w.stride <= 256 && o.hb * w.stride <= 256) o.tc_mode = 4;
@@ -1114,6 +1143,27 @@ hapi_status encode_bf16(CUtensorMap* map, int rank, void* base, const cuuint64_t
   return HAPI_OK;
 }
 
+// im2col map for mode 5: {C, W, H, N} NHWC view; the bounding box of traversal positions is
+// [-pad, dim - 1 + pad - (k - 1)] per spatial dim, walked with the conv stride, so a load at
+// (ow*s - pad, oh*s - pad, n) with tap offsets (s, r) yields the A tile of 128 consecutive
+// output pixels for that tap (padding = OOB zero fill); box = 64 channels x 128 pixels.
+hapi_status encode_im2col(hapi_model* m, void* base, const View& v, int C, int kh, int kw, int stride, int pad,
+                          CUtensorMap* map, const std::string& what) {
+  EncodeIm2colFn enc = get_im2col_fn();
+  if (!enc) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+  const cuuint64_t ld = (cuuint64_t)v.ld * 2;
+  cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)v.W, (cuuint64_t)v.H, (cuuint64_t)m->d.max_batch};
+  cuuint64_t strides[3] = {ld, ld * v.W, ld * v.W * v.H};
+  int lower[2] = {-pad, -pad};
+  int upper[2] = {pad - (kw - 1), pad - (kh - 1)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, lower, upper, 64, 128, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "im2col tensor map encode failed (%d): %s", (int)r, what.c_str());
+  return HAPI_OK;
+}
+
 // Map over an NHWC activation view with the conv's tile geometry: 2D [M][C] with a
 // {cols, 128} box for linear tiles, 4D {C, W, H, N} with a {cols, wb, hb, nb} box for
 // mode-4 spatial tiles.  The batch extent is max_batch.
@@ -1194,6 +1244,10 @@ hapi_status finalize_tmaps(hapi_model* m) {
         cuuint32_t estr[4] = {1, 1, 1, 1};
         st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " halo");
         if (st != HAPI_OK) return st;
+      } else if (o.tc_mode == 5) {
+        if ((st = encode_im2col(m, vptr(m, p, o.in, nullptr), o.in, w.cs, w.kh, w.kw, w.stride, w.pad, &o.tmap_a,
+                                o.desc + " A im2col")) != HAPI_OK)
+          return st;
       } else if (o.tc_mode == 3 || o.tc_mode == 4 || o.tc_mode == 7) {
         void* base = vptr(m, p, o.in, nullptr);
         const cuuint64_t es = 2, ld = (cuuint64_t)o.in.ld;
@@ -1213,7 +1267,11 @@ hapi_status finalize_tmaps(hapi_model* m) {
         }
         if (st != HAPI_OK) return st;
       }
-      if (o.dual) {
+      if (o.dual && o.tc_mode == 5) {
+        if ((st = encode_im2col(m, vptr(m, p, o.in2, nullptr), o.in2, w.cs2, 1, 1, w.stride2, 0, &o.tmap_a2,
+                                o.desc + " A2 im2col")) != HAPI_OK)
+          return st;
+      } else if (o.dual) {
         void* base2 = vptr(m, p, o.in2, nullptr);
         const cuuint64_t ld2 = (cuuint64_t)o.in2.ld * 2;
         if (o.tc_mode == 3) {
