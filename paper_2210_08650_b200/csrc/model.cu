@@ -553,9 +553,13 @@ struct Builder {
         if (w.kh == 1 && w.kw == 1 && w.stride == 1 && w.pad == 0) {
           o.tc_mode = 3;
         } else if (w.stride == 1 && w.kh > 1 && we <= 128 && halo_enabled() &&
-                   out.W * ((out.H + ((out.H + 128 / we - 1) / (128 / we)) - 1) / ((out.H + 128 / we - 1) / (128 / we))) >= 96) {
-          // halo mode: one input box per 64-channel block, taps from row-shifted descriptors
-          // (only when a tile keeps >= 96 of its 128 rows valid; 7x7 maps use mode 4)
+                   out.W * ((out.H + ((out.H + 128 / we - 1) / (128 / we)) - 1) / ((out.H + 128 / we - 1) / (128 / we))) >=
+                       (w.bn >= 128 && !res && im2col_enabled() ? 108 : 96)) {
+          // halo mode: one input box per 64-channel block, taps from row-shifted descriptors.
+          // Only when a tile keeps enough of its 128 rows valid: measured on ResNet-50, halo beats
+          // im2col at 116 and 112 valid rows (stage 1 -47%, stage 2 -18%) but loses at 98 (stage 3
+          // 14x14: +10%); narrow-N convs stay on halo (their MMA is smem-bound, and im2col writes
+          // 9x the A bytes into smem), and so do residual convs (ResNet-18 stage 3: 2x slower on im2col)
           const int hmax = 128 / we;
           const int tiles_h = (out.H + hmax - 1) / hmax;
           o.hb = (out.H + tiles_h - 1) / tiles_h;
