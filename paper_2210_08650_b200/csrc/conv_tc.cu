@@ -284,10 +284,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
       for (int kc = 0; kc < g.k_chunks; ++kc) {
         const int c0 = kc * BK + j * 8;
-        const float4 s0 = *reinterpret_cast<const float4*>(sScale + c0);
-        const float4 s1 = *reinterpret_cast<const float4*>(sScale + c0 + 4);
-        const float4 h0 = *reinterpret_cast<const float4*>(sShift + c0);
-        const float4 h1 = *reinterpret_cast<const float4*>(sShift + c0 + 4);
+        const float4 s0 = lds_f4(smem_u32(sScale + c0));
+        const float4 s1 = lds_f4(smem_u32(sScale + c0 + 4));
+        const float4 h0 = lds_f4(smem_u32(sShift + c0));
+        const float4 h1 = lds_f4(smem_u32(sShift + c0 + 4));
         const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
         const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
         mbar_wait(&lfull[stage], phase);
@@ -917,8 +917,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int c4 = 0; c4 < 4; ++c4) {  // 8 columns = one 16-byte chunk
               const int chunk = sub * 4 + c4;
               float f[8];
+              {
+                const uint32_t ba = smem_u32(sBias + jb + chunk * 8);
+                const float4 b0 = lds_f4(ba), b1 = lds_f4(ba + 16);
+                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-              for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c4 * 8 + j]) + sBias[jb + chunk * 8 + j];
+                for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c4 * 8 + j]) + bb[j];
+              }
               if (srow < 0) continue;
               if (g.has_res) {
                 uint32_t r0, r1, r2, r3;
