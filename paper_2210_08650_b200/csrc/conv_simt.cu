@@ -47,7 +47,25 @@ __global__ void __launch_bounds__(256)
   const int b_n = (tid & 15) * 4;
 
   float ra[4], rb[4];
+  // fast path (C % 16 == 0, 16-byte aligned rows): a 16-wide K tile lies inside one filter tap,
+  // so each thread's 4 consecutive channels are one bounds check and one float4 load
+  const bool fast = (a.C % TK == 0) && (a.x_ld % 4 == 0) && (a.Cout % 4 == 0) && !a.pro_scale;
   auto load_tile = [&](int k0) {
+    if (fast) {
+      const int tap = k0 / a.C;
+      const int c = k0 - tap * a.C + a_k;
+      const int r = tap / a.KW, s = tap - (tap / a.KW) * a.KW;
+      const int ih = ih0 + r, iw = iw0 + s;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k0 < a.K && (unsigned)ih < (unsigned)a.H && (unsigned)iw < (unsigned)a.W)
+        v = __ldg(reinterpret_cast<const float4*>(x + (ioff + (long long)ih * a.W + iw) * a.x_ld + c));
+      ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
+      const int kb = k0 + b_k;
+      float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kb < a.K && n_base + b_n < a.Cout) u = __ldg(reinterpret_cast<const float4*>(w + (long long)kb * a.Cout + n_base + b_n));
+      rb[0] = u.x; rb[1] = u.y; rb[2] = u.z; rb[3] = u.w;
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int k = k0 + a_k + j;
@@ -80,13 +98,19 @@ __global__ void __launch_bounds__(256)
 
   const int ty = tid >> 4, tx = tid & 15;
   float acc[4][4] = {};
-  const int nk = (a.K + TK - 1) / TK;
-  load_tile(0);
+  // K slice of this CTA (split-K: blockIdx.z of ksplit; slices are whole TK tiles)
+  const int nk_all = (a.K + TK - 1) / TK;
+  const int ks = a.ksplit > 1 ? a.ksplit : 1;
+  const int per = (nk_all + ks - 1) / ks;
+  const int kt0 = blockIdx.z * per;
+  const int nk = (kt0 + per < nk_all ? kt0 + per : nk_all) - kt0;
+  if (nk > 0) {
+  load_tile(kt0 * TK);
   store_tile(0);
   __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
     const int cur = kt & 1;
-    if (kt + 1 < nk) load_tile((kt + 1) * TK);
+    if (kt + 1 < nk) load_tile((kt0 + kt + 1) * TK);
 #pragma unroll
     for (int kk = 0; kk < TK; ++kk) {
       float av[4], bv[4];
@@ -101,6 +125,22 @@ __global__ void __launch_bounds__(256)
     }
     if (kt + 1 < nk) store_tile(cur ^ 1);
     __syncthreads();
+  }
+  }
+  if (ks > 1) {
+    // raw partial sums; the reduce kernel applies the epilogue
+    float* wz = a.ws + (long long)blockIdx.z * a.M * a.Cout;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long m = m_base + ty * 4 + i;
+      if (m >= a.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = n_base + tx * 4 + j;
+        if (n < a.Cout) wz[m * a.Cout + n] = acc[i][j];
+      }
+    }
+    return;
   }
 
   float* y = static_cast<float*>(a.y);
@@ -130,14 +170,58 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+
+// out = epilogue(sum over slices, in slice order) -- one thread per output element
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const ConvArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const long long total = a.M * a.Cout;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  float* y = static_cast<float*>(a.y);
+  const float* res = static_cast<const float*>(a.res);
+  const int OHW = a.OH * a.OW;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const long long m = e / a.Cout;
+    const int n = (int)(e - m * a.Cout);
+    float v = 0.f;
+    for (int z = 0; z < a.ksplit; ++z) v += a.ws[(long long)z * total + e];
+    if (a.bias) v += __ldg(a.bias + n);
+    if (res) v += __ldg(res + m * a.res_ld + n);
+    if (a.relu) v = fmaxf(v, 0.f);
+    if (a.nchw) {
+      const int img = (int)(m / OHW), pix = (int)(m - (long long)img * OHW);
+      y[((long long)img * a.Cout + n) * OHW + pix] = v;
+    } else {
+      y[m * a.y_ld + n] = v;
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t conv_simt_launch(const ConvArgs& a, cudaStream_t st) {
   const long long mt = (a.M + TM - 1) / TM;
   const int nt = (a.Cout + TN - 1) / TN;
   if (mt <= 0 || nt <= 0) return cudaSuccess;
-  dim3 grid((unsigned)mt, (unsigned)nt);
-  return launch_pdl(conv_simt_kernel, grid, dim3(256), 0, st, a);
+  const int ks = a.ksplit > 1 && a.ws ? a.ksplit : 1;
+  dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)ks);
+  ConvArgs b = a;
+  b.ksplit = ks;
+  cudaError_t e = launch_pdl(conv_simt_kernel, grid, dim3(256), 0, st, b);
+  if (e != cudaSuccess || ks == 1) return e;
+  const long long total = a.M * a.Cout;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  return launch_pdl(splitk_reduce_kernel, dim3((unsigned)blocks), dim3(256), 0, st, b);
+}
+
+int conv_simt_ksplit(long long M, int Cout, int K, int num_sms) {
+  // split K when the output grid leaves most of the GPU idle (small batches: config 1)
+  const long long tiles = ((M + TM - 1) / TM) * ((Cout + TN - 1) / TN);
+  const int nk = (K + TK - 1) / TK;
+  int ks = 1;
+  while (ks < 8 && tiles * ks < 2LL * num_sms && nk / (ks * 2) >= 16) ks *= 2;
+  return ks;
 }
 
 }  // namespace hapi

@@ -75,6 +75,11 @@ struct ConvArgs {
   // output) against an identity weight block; each N tile multiplies only its diagonal
   // BN-channel block (k2_chunks = BN / 64 chunks per tile)
   int k2_diag;
+  // fp32 SIMT path: split-K over `ksplit` slices (small grids); raw partial sums go to
+  // ws [ksplit][M][Cout] fp32 and a second kernel adds them in slice order (deterministic)
+  // with the bias / residual / ReLU epilogue
+  int ksplit;
+  float* ws;
 };
 
 // tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).  A-operand modes:
@@ -122,6 +127,8 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& maps, int bn, int 
 
 // SIMT fp32 path (weights packed [K][Cout] fp32).
 cudaError_t conv_simt_launch(const ConvArgs& a, cudaStream_t st);
+// split-K factor for a small SIMT conv grid (1 = no split)
+int conv_simt_ksplit(long long M, int Cout, int K, int num_sms);
 
 // NCHW fp32 images -> NHWC activations.  layout 0: fp32, C=3.  layout 1: bf16, C=8
 // (channels 3..7 zero).  layout 2: bf16 space-to-depth 2x2 with a zero border ->

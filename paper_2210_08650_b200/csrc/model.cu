@@ -187,6 +187,8 @@ struct Op {
   View out2;
   CUtensorMap tmap_b1;           // conv3 weights with a {64, 128} box
   CUtensorMap tmap_y2;
+  int ksplit = 1;                // fp32 SIMT split-K slices (partial sums in `ws`)
+  View ws;
 };
 
 struct Buf {
@@ -898,6 +900,32 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     }
   }
 
+  // fp32 path: split K of convs whose output grid would leave most SMs idle (small batches,
+  // config 1).  The [ksplit][M][Cout] workspace is an arena buffer live only during the conv,
+  // capped so that in + out + workspace stays within the plan's largest in + out (the
+  // per-image peak the planner's P(s) already covers, section 4.3).
+  if (!m->bf16) {
+    std::vector<Op>& ops = b.p.ops;
+    double peak = 0;
+    for (const Op& o : ops)
+      if (o.t == OP_CONV)
+        peak = std::max(peak, ((double)o.in.H * o.in.W * o.in.ld + (double)o.out.H * o.out.W * o.out.ld) * m->es);
+    for (size_t k = 0; k < ops.size(); ++k) {
+      if (ops[k].t != OP_CONV) continue;
+      const ConvW& w = m->convs[ops[k].conv];
+      const View in = ops[k].in, out = ops[k].out;
+      int ks = conv_simt_ksplit((long long)m->d.max_batch * out.H * out.W, w.cout, w.K, m->num_sms);
+      const double io = ((double)in.H * in.W * in.ld + (double)out.H * out.W * out.ld) * m->es;
+      const double wsb = (double)out.H * out.W * w.cout * m->es;
+      while (ks > 1 && io + ks * wsb > peak) ks /= 2;
+      if (ks > 1) {
+        View ws = b.compact(w.cout * ks, out.H, out.W);
+        ops[k].ksplit = ks;
+        ops[k].ws = ws;
+      }
+    }
+  }
+
   // Peephole: a bottleneck's last conv (1x1, residual or stride-1 downsample as second A
   // source) directly followed by the next block's 1x1 conv1 reading its output becomes one
   // OP_PAIR launch -- the block output tile stays in smem as conv1's A operand.
@@ -966,6 +994,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     if (o.dual) touch(o.in2.buf);
     touch(o.out.buf);
     if (o.t == OP_PAIR) touch(o.out2.buf);
+    if (o.ksplit > 1) touch(o.ws.buf);
   }
   const int64_t B = m->d.max_batch;
   std::vector<int> order;
@@ -1079,6 +1108,8 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
         e = conv_tc_launch(a, mp, w.bn, o.tc_mode, o.wb, o.hb, o.nb, m->num_sms, st);
       } else {
+        a.ksplit = o.ksplit;
+        a.ws = o.ksplit > 1 ? reinterpret_cast<float*>(vptr(m, p, o.ws, out)) : nullptr;
         e = conv_simt_launch(a, st);
       }
       break;
