@@ -100,6 +100,8 @@ struct Geo {
   int ring_bytes;                   // mode 8: M8_RING stem rows x (2 pq + 1) pixels x 128 B
   int res_depth;                    // residual ring depth (blocks of [128 x SB] in flight)
   int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
+  int mc;                           // 1: 2-CTA cluster, each weight chunk multicast to both CTAs
+  int n_pairs;                      // mc: (M-tile pair, N tile) work items
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -134,6 +136,14 @@ __device__ __forceinline__ int tile_at(const Geo& g, int k, int num_tiles) {
     const int task = blockIdx.x + (k / g.ph) * gridDim.x;
     return task < g.n_tasks ? task * g.ph + (k - (k / g.ph) * g.ph) : -1;
   }
+  if (g.mc) {
+    // the two CTAs of a cluster walk the same (M-tile pair, N tile) items in lockstep, rank r
+    // taking M tile 2p + r (beyond the last tile: OOB loads read zeros, stores are clipped)
+    const int q = (int)(blockIdx.x >> 1) + k * (int)(gridDim.x >> 1);
+    if (q >= g.n_pairs) return -1;
+    const int tp = q / g.n_tiles, tn = q - tp * g.n_tiles;
+    return (2 * tp + (int)(blockIdx.x & 1)) * g.n_tiles + tn;
+  }
   const int t = blockIdx.x + k * gridDim.x;
   return t < num_tiles ? t : -1;
 }
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const ConvArgs a, const Geo g, const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_y,
                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2,
-                   const __grid_constant__ CUtensorMap tmap_b2) {
+                   const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_bh) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
   // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
@@ -209,7 +219,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], MODE == 7 ? NUM_PROD_THREADS : (TMA_A ? 1 : NUM_PROD_THREADS + 1));
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], g.mc ? 2 : 1);  // mc: both CTAs' MMAs release the multicast stage
       mbar_init(&lfull[s], 1);
     }
     for (int i = 0; i < MAX_A_STAGES; ++i) {
@@ -243,6 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (g.mc) cluster_sync_all();  // peers' barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   griddep_wait();  // the previous kernel's outputs are visible from here on
@@ -549,6 +560,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   const uint32_t dB = smem_u32(sB + stage * BSZ + j * C::B_STAGE_BYTES);
                   if (a.k2_diag && ck >= g.k1_chunks)
                     tma_load_2d(dB, &tmap_b2, (ck - g.k1_chunks) * BK, 0, &full[stage]);
+                  else if (g.mc)  // my half of the weight chunk, multicast into both CTAs
+                    tma_load_2d_mc(dB + (blockIdx.x & 1) * (BN / 2) * 128, &tmap_bh, ck * BK,
+                                   tn * BN + (int)(blockIdx.x & 1) * (BN / 2), &full[stage], 3);
                   else
                     tma_load_2d(dB, &tmap_b, ck * BK, tn * BN, &full[stage]);
                 }
@@ -803,7 +817,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kc + j) | k) != 0);
               }
             }
-            mma_commit(&empty[stage]);
+            if (g.mc)
+              mma_commit_mc(&empty[stage], 3);  // both CTAs' producers refill this multicast stage
+            else
+              mma_commit(&empty[stage]);
             if (kc + nch >= g.k_chunks) mma_commit(&tfull[acc]);
           }
           __syncwarp();
@@ -977,6 +994,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (g.mc) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS * MT)
@@ -987,6 +1005,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 bool bres_enabled() {  // HAPI_BRES=1: also keep weights resident in modes 3/4 (experiment)
   static const bool on = [] {
     const char* e = std::getenv("HAPI_BRES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+// 2-CTA weight multicast is correct (parity-tested) but measured neutral-to-slower on
+// ResNet-50 b512 (+1.5%: the weight stream is not the limiter), so it is opt-in: HAPI_CLUSTER=1.
+bool cluster_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_CLUSTER");
     return e && e[0] == '1';
   }();
   return on;
@@ -1058,13 +1086,40 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
     smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes + pro_bytes;
   }
   if (g.stages < 2 && !(g.mode == 6 && g.b_res)) return cudaErrorInvalidValue;
-  const int tiles = g.mode == 8 ? g.n_tasks : (g.m_tiles + g.mt - 1) / g.mt * g.n_tiles;
-  const int grid = tiles < num_sms ? tiles : num_sms;
+  // 2-CTA clusters with multicast weights: the generic TMA path, weights streamed (not
+  // resident), no identity block, at least two M tiles; every weight chunk then crosses L2
+  // once per CTA pair instead of once per CTA
+  g.mc = 0;
+  if ((g.mode == 3 || g.mode == 4 || g.mode == 5) && !g.b_res && !a.k2_diag && BN >= 128 && mp.bh &&
+      g.m_tiles >= 2 && cluster_enabled()) {
+    g.mc = 1;
+    g.n_pairs = (g.m_tiles + 1) / 2 * g.n_tiles;
+  }
+  const int tiles = g.mode == 8 ? g.n_tasks : g.mc ? 2 * g.n_pairs : (g.m_tiles + g.mt - 1) / g.mt * g.n_tiles;
+  int grid = tiles < num_sms ? tiles : num_sms;
+  if (g.mc) grid &= ~1;
   if (grid <= 0) return cudaSuccess;
   const CUtensorMap* b = mp.b;
-  return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
-                    mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b,
-                    mp.b2 ? *mp.b2 : *b);
+  if (!g.mc)
+    return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
+                      mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b,
+                      mp.b2 ? *mp.b2 : *b, *b);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, MODE>, a, g, mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b,
+                            mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b, mp.b2 ? *mp.b2 : *b, *mp.bh);
 }
 
 template <int BN>

@@ -94,6 +94,7 @@ struct ConvMaps {
   const CUtensorMap* a2; // second A source (k2_chunks > 0) or nullptr
   const CUtensorMap* b2; // k2_diag: the shared 256x256 bf16 identity, box {64, BN}
   const CUtensorMap* b;  // weights
+  const CUtensorMap* bh; // weights with a {64, bn/2} box (2-CTA multicast halves) or nullptr
   const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
   const CUtensorMap* r;  // residual view or nullptr
 };

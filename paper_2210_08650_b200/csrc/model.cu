@@ -146,6 +146,8 @@ struct ConvW {
   float* pro_scale = nullptr;  // [cs]
   float* pro_shift = nullptr;
   CUtensorMap tmap;
+  CUtensorMap tmap_half;         // {64, bn/2} box: each CTA of a 2-CTA cluster loads one half
+  bool has_half = false;
   int bn = 0, mode = 0;
   double real_flops_per_px = 0;  // 2 * K_real * Cout
   int K2 = 0, cs2 = 0, stride2 = 1;  // fused downsample source (bf16): 1x1/stride2 over cs2 channels
@@ -463,6 +465,14 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for %s", (int)r, s.wname.c_str());
+    if (cw.bn >= 128) {
+      cuuint32_t boxh[2] = {64, (cuuint32_t)(cw.bn / 2)};
+      r = enc(&cw.tmap_half, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, cw.w, dims, strides, boxh, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for %s", (int)r, s.wname.c_str());
+      cw.has_half = true;
+    }
   } else {
     cw.Kp = cw.K;
     std::vector<float> hw((size_t)cw.K * s.cout, 0.f);
@@ -1104,6 +1114,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
         mp.a2 = o.dual ? &o.tmap_a2 : nullptr;
         mp.b2 = w.res_identity ? (w.bn == 256 ? &m->ident_map256 : &m->ident_map128) : nullptr;
         mp.b = &w.tmap;
+        mp.bh = w.has_half ? &w.tmap_half : nullptr;
         mp.y = o.nchw_out ? nullptr : &o.tmap_y;
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
         e = conv_tc_launch(a, mp, w.bn, o.tc_mode, o.wb, o.hb, o.nb, m->num_sms, st);
