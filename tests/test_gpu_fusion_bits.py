@@ -1,4 +1,4 @@
-"""Fusions that must not change a single output bit (GPU).
+"""Fusions and scheduling variants that must not change a single output bit (GPU).
 
 The chained conv3 -> next-conv1 pair kernel (conv_pair.cu) keeps the block output tile in
 shared memory instead of re-reading it, but every GEMM sees the same bf16 operands in the same
@@ -41,16 +41,18 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("arch,split,size,n,flag", [
-    ("resnet50", 21, 96, 6, "HAPI_PAIR"),        # pair kernel (stage 1 ds/identity pairs, stage 2 pairs)
-    ("resnet50", 9, 64, 5, "HAPI_PAIR"),         # split right after a paired block boundary
-    ("resnet50", 21, 96, 6, "HAPI_STEM_POOL"),   # stem conv + maxpool fusion
-    ("densenet121", 9, 64, 5, "HAPI_STEM_POOL"),
-    ("resnet50", 21, 96, 6, "HAPI_DUAL_M"),      # two M sub-tiles per weight stage (halo mode)
+@pytest.mark.parametrize("arch,split,size,n,flag,on,off", [
+    ("resnet50", 21, 96, 6, "HAPI_PAIR", None, "0"),        # pair kernel (stage 1/2 pairs)
+    ("resnet50", 9, 64, 5, "HAPI_PAIR", None, "0"),         # split right after a paired block boundary
+    ("resnet50", 21, 96, 6, "HAPI_STEM_POOL", None, "0"),   # stem conv + maxpool fusion
+    ("densenet121", 9, 64, 5, "HAPI_STEM_POOL", None, "0"),
+    ("resnet50", 21, 96, 6, "HAPI_DUAL_M", None, "0"),      # two M sub-tiles per weight stage (halo mode)
+    ("resnet50", 21, 96, 6, "HAPI_CLUSTER", "1", None),     # 2-CTA multicast weights (opt-in)
+    ("resnet50", 21, 160, 3, "HAPI_CLUSTER", "1", None),    # ... odd M-tile count (OOB pair tile)
 ])
-def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag):
-    fused = _run(tmp_path, {}, arch, split, size, n, "on")
-    plain = _run(tmp_path, {flag: "0"}, arch, split, size, n, "off")
+def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off):
+    fused = _run(tmp_path, {flag: on} if on else {}, arch, split, size, n, "on")
+    plain = _run(tmp_path, {flag: off} if off else {}, arch, split, size, n, "off")
     assert fused.shape == plain.shape
     assert np.array_equal(fused.view(np.uint32), plain.view(np.uint32)), (
         flag, int((fused != plain).sum()), float(np.abs(fused - plain).max()))
