@@ -112,6 +112,43 @@ typedef struct {
  * does not fit.  All arithmetic u64 with overflow -> INVALID_ARGUMENT.  Pure. */
 HAPI_API hapi_status hapi_choose_split(const hapi_split_query *q, hapi_split_result *r, uint32_t *candidates);
 
+/* ------------------------------------------------------------ batch adaptation (host)
+ * Section 4.5: the COS batch of every queued
+ * request of one GPU from Eq. 4,
+ *     max sum_r b_r*M_r(data) + M_r(model)
+ *     s.t. b_min,r <= b_r <= b_max,r,   sum_r b_r*M_r(data) + M_r(model) <= available_bytes,
+ * with M_r(model) = W(s_r) and M_r(data) = P(s_r) from hapi_layer_sizes, and
+ * available_bytes = M_total - M(occupied).  The paper states the problem, not a solver;
+ * readings:
+ *   F1 infeasible -> requests are removed one at a time, most recent arrival first
+ *      ("removes one request at a time and retries"); they get batch 0
+ *      (deferred to the next run), so the deferred set is a suffix of arrival order;
+ *   F2 solver = unit water-filling: every kept request starts at b_min, then one more sample
+ *      goes to the request with the smallest current b (earliest arrival on ties) that is below
+ *      b_max and whose M(data) still fits, until none does -- the objective is within
+ *      max_r M_r(data) of the optimum;
+ *   F3 max_concurrency > 0 (the static cap) defers every request beyond the
+ *      first max_concurrency by arrival; 0 = no cap;
+ *   F4 hapi_partition_requests spreads requests (in arrival order) round-robin over GPUs
+ *      ("distributes requests evenly on the existing GPUs").
+ * Pure, deterministic, no device work. */
+typedef struct {
+  uint64_t arrival_seq;           /* arrival order key (ties: input order) */
+  uint64_t model_bytes;           /* M_r(model) */
+  uint64_t data_bytes;            /* M_r(data) per sample */
+  uint32_t b_min, b_max;          /* 1 <= b_min <= b_max (b_min = 25 in the paper) */
+} hapi_adapt_request;
+
+/* batch[i] <- b_i (0 = deferred) for the n requests in input order; *used_bytes (may be NULL)
+ * <- memory of the kept requests.  Errors: INVALID_ARGUMENT (null arrays with n > 0, bad
+ * bounds).  n = 0 is valid (nothing assigned, 0 bytes). */
+HAPI_API hapi_status hapi_adapt_batches(const hapi_adapt_request *reqs, uint32_t n, uint64_t available_bytes,
+                                        uint32_t max_concurrency, uint32_t *batch, uint64_t *used_bytes);
+
+/* gpu_of[i] <- GPU of the i-th request in arrival order (round-robin, F4).  Errors:
+ * INVALID_ARGUMENT (n_gpus = 0, null gpu_of with n > 0). */
+HAPI_API hapi_status hapi_partition_requests(uint32_t n, uint32_t n_gpus, uint32_t *gpu_of);
+
 /* Parameters expected by hapi_model_create, in torchvision state_dict order
  * (num_batches_tracked buffers excluded): count, and per index the name (copied into
  * name_buf, NUL-terminated, truncated to name_cap) and shape (dims[4], *ndim). */

@@ -137,3 +137,66 @@ def estimate(arch: str, split_idx: int, batch: int, act: str = "f32", in_h: int 
     """est(b, s) = W(s) + b * P(s)."""
     sz = layer_sizes(arch, in_h, in_w, act)
     return _u64(sz.weight_bytes[split_idx - 1] + batch * sz.peak_bytes[split_idx - 1])
+
+
+# ---------------------------------------------------------------- section 4.5 (SURVEY 8(f) f1)
+# Multi-request batch adaptation, Eq. 4 (PAPER.md:846-860) over all queued requests of one
+# GPU:  maximise sum_r b_r * M_r(data) + M_r(model)  s.t.  b_min,r <= b_r <= b_max,r  and
+# sum_r (b_r * M_r(data) + M_r(model)) <= M_total - M_occupied.  The paper gives the problem,
+# not a solver; readings (DESIGN.md, F1-F4):
+#   F1 infeasible -> "removes one request at a time and retries" (PAPER.md:864): the most
+#      recently arrived request is deferred first (deferred ids are a suffix of arrival order);
+#   F2 solver: unit water-filling -- start every request at b_min, then repeatedly give one
+#      more sample to the request with the smallest current b (ties: earliest arrival) that is
+#      below its b_max and whose M_r(data) still fits; stop when none does.  The objective is
+#      then within max_r M_r(data) of the optimum (every request is at b_max or cannot grow);
+#   F3 the static concurrency cap ("capped statically", PAPER.md:866) defers the requests
+#      beyond the first `max_concurrency` by arrival before the memory check;
+#   F4 requests are spread over GPUs round-robin by arrival ("distributes requests evenly",
+#      PAPER.md:862), and the adaptation runs per GPU.
+
+@dataclass
+class AdaptRequest:
+    arrival_seq: int
+    model_bytes: int         # M_r(model) = W(s)
+    data_bytes: int          # M_r(data) per sample = P(s)
+    b_min: int
+    b_max: int
+
+
+def adapt_batches(reqs: List[AdaptRequest], available: int, max_concurrency: int = 0):
+    """-> (batch per request in input order, 0 = deferred; memory used)."""
+    for r in reqs:
+        if not (1 <= r.b_min <= r.b_max):
+            raise ValueError("b_min/b_max")
+    order = sorted(range(len(reqs)), key=lambda i: (reqs[i].arrival_seq, i))
+    active = order[:max_concurrency] if max_concurrency > 0 else list(order)
+
+    def floor_need(ids):
+        return sum(reqs[i].b_min * reqs[i].data_bytes + reqs[i].model_bytes for i in ids)
+
+    while active and floor_need(active) > available:
+        active.pop()                                  # most recent arrival first (F1)
+    b = [0] * len(reqs)
+    for i in active:
+        b[i] = reqs[i].b_min
+    rem = available - floor_need(active) if active else available
+    while True:
+        best = None
+        for i in active:                              # arrival order: first minimum wins ties
+            r = reqs[i]
+            if b[i] < r.b_max and r.data_bytes <= rem and (best is None or b[i] < b[best]):
+                best = i
+        if best is None:
+            break
+        b[best] += 1
+        rem -= reqs[best].data_bytes
+    used = sum(b[i] * reqs[i].data_bytes + reqs[i].model_bytes for i in active)
+    return b, used
+
+
+def partition_requests(n: int, n_gpus: int) -> List[int]:
+    """GPU of each request (requests given in arrival order): round-robin (F4)."""
+    if n_gpus < 1:
+        raise ValueError("n_gpus")
+    return [i % n_gpus for i in range(n)]

@@ -77,6 +77,25 @@ def hapi_choose_split(arch, freeze_idx: int, training_batch: int, link_bytes_per
     return ("ok" if st == 0 else "infeasible"), res, list(cands)[: r.n_candidates]
 
 
+def hapi_adapt_batches(requests, available_bytes: int, max_concurrency: int = 0):
+    """Section 4.5 batch adaptation (Eq. 4 over queued requests).  requests: iterable of
+    (arrival_seq, model_bytes, data_bytes, b_min, b_max).  Returns (batches, used_bytes);
+    batch 0 = deferred."""
+    reqs = list(requests)
+    arr = (_lib.AdaptRequest * max(len(reqs), 1))(*[_lib.AdaptRequest(*r) for r in reqs])
+    out = (_lib.u32 * max(len(reqs), 1))()
+    used = _lib.u64()
+    _check(_lib.hapi_adapt_batches(arr, len(reqs), available_bytes, max_concurrency, out, C.byref(used)))
+    return list(out)[: len(reqs)], used.value
+
+
+def hapi_partition_requests(n: int, n_gpus: int):
+    """GPU of each request in arrival order (round-robin)."""
+    out = (_lib.u32 * max(n, 1))()
+    _check(_lib.hapi_partition_requests(n, n_gpus, out))
+    return list(out)[:n]
+
+
 def hapi_param_table(arch):
     """[(name, shape)] the library expects, in torchvision state_dict order."""
     n = _lib.hapi_num_params(_arch(arch))

@@ -29,6 +29,10 @@ class SplitResult(C.Structure):
                 ("n_candidates", u32)]
 
 
+class AdaptRequest(C.Structure):
+    _fields_ = [("arrival_seq", u64), ("model_bytes", u64), ("data_bytes", u64), ("b_min", u32), ("b_max", u32)]
+
+
 class ModelDesc(C.Structure):
     _fields_ = [("arch", C.c_int), ("act", C.c_int), ("in_h", u32), ("in_w", u32), ("min_split", u32),
                 ("max_split", u32), ("max_batch", u32), ("device", C.c_int)]
@@ -45,6 +49,8 @@ hapi_num_layers = _sig("hapi_num_layers", i32, C.c_int)
 hapi_freeze_index = _sig("hapi_freeze_index", i32, C.c_int)
 hapi_layer_sizes = _sig("hapi_layer_sizes", C.c_int, C.c_int, u32, u32, C.c_int, P_u64, P_u64, P_u64, P_u64, u32)
 hapi_choose_split = _sig("hapi_choose_split", C.c_int, C.POINTER(SplitQuery), C.POINTER(SplitResult), P_u32)
+hapi_adapt_batches = _sig("hapi_adapt_batches", C.c_int, C.POINTER(AdaptRequest), u32, u64, u32, P_u32, P_u64)
+hapi_partition_requests = _sig("hapi_partition_requests", C.c_int, u32, u32, P_u32)
 hapi_num_params = _sig("hapi_num_params", i32, C.c_int)
 hapi_param_info = _sig("hapi_param_info", C.c_int, C.c_int, u32, C.c_char_p, u32, C.POINTER(i64), P_u32)
 hapi_model_create = _sig("hapi_model_create", C.c_int, C.POINTER(ModelDesc), C.POINTER(C.c_void_p), u32,
@@ -61,7 +67,8 @@ hapi_model_destroy = _sig("hapi_model_destroy", None, C.c_void_p)
 hapi_last_error = _sig("hapi_last_error", C.c_char_p)
 hapi_build_info = _sig("hapi_build_info", C.c_char_p)
 
-EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_choose_split", "hapi_num_params",
+EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_choose_split", "hapi_adapt_batches",
+            "hapi_partition_requests", "hapi_num_params",
             "hapi_param_info", "hapi_model_create", "hapi_model_set_stream", "hapi_prefix_forward",
             "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_plan_describe", "hapi_prefix_forward_timed",
             "hapi_model_destroy", "hapi_last_error", "hapi_build_info"]

@@ -3,7 +3,9 @@
 // choice and Eq. 4's single-request COS batch.
 // Pure integer host code; u64 with overflow checks.
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "arch.h"
@@ -167,6 +169,74 @@ hapi_status hapi_param_info(hapi_arch arch, uint32_t idx, char* name_buf, uint32
   }
   if (dims) for (int i = 0; i < 4; ++i) dims[i] = i < p.ndim ? p.dims[i] : 0;
   if (ndim) *ndim = (uint32_t)p.ndim;
+  return HAPI_OK;
+}
+
+// Section 4.5 batch adaptation: Eq. 4 over the queued requests of one GPU,
+// readings F1-F4 in include/hapi.h.  Host-only, pure.
+hapi_status hapi_adapt_batches(const hapi_adapt_request* reqs, uint32_t n, uint64_t available_bytes,
+                               uint32_t max_concurrency, uint32_t* batch, uint64_t* used_bytes) {
+  clear_error();
+  if (n > 0 && (!reqs || !batch)) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null requests/batch");
+  for (uint32_t i = 0; i < n; ++i)
+    if (reqs[i].b_min < 1 || reqs[i].b_min > reqs[i].b_max)
+      return set_error(HAPI_ERR_INVALID_ARGUMENT, "request %u: b_min/b_max", i);
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t x, uint32_t y) { return reqs[x].arrival_seq < reqs[y].arrival_seq; });
+  if (max_concurrency > 0 && order.size() > max_concurrency) order.resize(max_concurrency);  // F3
+  // floor footprint sum_r (b_min * data + model); u64 with overflow treated as "does not fit"
+  auto floor_need = [&](const std::vector<uint32_t>& ids, uint64_t* out) {
+    uint64_t t = 0;
+    for (uint32_t i : ids) {
+      uint64_t x;
+      if (!mul_ok(reqs[i].b_min, reqs[i].data_bytes, &x) || !add_ok(x, reqs[i].model_bytes, &x) || !add_ok(t, x, &t))
+        return false;
+    }
+    *out = t;
+    return true;
+  };
+  uint64_t need = 0;
+  while (!order.empty() && (!floor_need(order, &need) || need > available_bytes)) order.pop_back();  // F1
+  for (uint32_t i = 0; i < n; ++i) batch[i] = 0;
+  uint64_t rem = available_bytes;
+  if (!order.empty()) {
+    rem -= need;
+    for (uint32_t i : order) batch[i] = reqs[i].b_min;
+    // F2 unit water-filling: one more sample to the smallest b (earliest arrival on ties) that
+    // is below its b_max and whose M(data) still fits.  Granted here a level at a time: the
+    // winner keeps winning unit steps until it reaches an earlier-arrived rival's b, or passes
+    // a later-arrived rival's b by one, so those unit steps are applied at once.
+    std::vector<uint32_t> pos(n, 0);
+    for (uint32_t k = 0; k < order.size(); ++k) pos[order[k]] = k;
+    for (;;) {
+      int64_t best = -1;
+      for (uint32_t i : order) {  // arrival order: the first minimum wins ties
+        const hapi_adapt_request& r = reqs[i];
+        if (batch[i] < r.b_max && r.data_bytes <= rem && (best < 0 || batch[i] < batch[best])) best = i;
+      }
+      if (best < 0) break;
+      uint64_t next = reqs[best].b_max;
+      for (uint32_t i : order) {
+        if ((int64_t)i == best || batch[i] >= reqs[i].b_max || reqs[i].data_bytes > rem) continue;
+        next = std::min<uint64_t>(next, (uint64_t)batch[i] + (pos[i] < pos[best] ? 0 : 1));
+      }
+      uint64_t grant = next - batch[best];  // >= 1 (see above)
+      if (reqs[best].data_bytes > 0) grant = std::min<uint64_t>(grant, rem / reqs[best].data_bytes);
+      batch[best] += (uint32_t)grant;
+      rem -= grant * reqs[best].data_bytes;
+    }
+  }
+  if (used_bytes) *used_bytes = available_bytes - rem;
+  return HAPI_OK;
+}
+
+hapi_status hapi_partition_requests(uint32_t n, uint32_t n_gpus, uint32_t* gpu_of) {
+  clear_error();
+  if (n_gpus < 1) return set_error(HAPI_ERR_INVALID_ARGUMENT, "n_gpus = 0");
+  if (n > 0 && !gpu_of) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null gpu_of");
+  for (uint32_t i = 0; i < n; ++i) gpu_of[i] = i % n_gpus;  // F4 round-robin by arrival
   return HAPI_OK;
 }
 
