@@ -194,6 +194,24 @@ HAPI_API hapi_status hapi_model_set_stream(hapi_model *m, void *cuda_stream);
 HAPI_API hapi_status hapi_prefix_forward(hapi_model *m, uint32_t split_idx, const float *images,
                                 uint64_t batch, void *out);
 
+/* Client-side frozen suffix ("the client ... runs the
+ * remaining layers", PAPER.md:902-906 frozen layers up to the freeze index): a model whose
+ * input is layer `start_idx`'s output in the send-buffer layout (contiguous NCHW, act dtype,
+ * exactly what hapi_prefix_forward writes at split = start_idx) and which computes layers
+ * start_idx+1 .. end_idx for end_idx in [min_split, max_split].  Same kernels and fusions as
+ * the prefix; weights of layers <= start_idx are never read.  Requires
+ * 1 <= start_idx < min_split; everything else as hapi_model_create.  Such a model only
+ * accepts hapi_suffix_forward (the prefix entry points return INVALID_ARGUMENT). */
+HAPI_API hapi_status hapi_model_create_suffix(const hapi_model_desc *desc, uint32_t start_idx,
+                                              const float *const *params, uint32_t n_params, hapi_model **out);
+
+/* acts: device [batch, layer start_idx output] (act dtype, contiguous NCHW); out: device,
+ * batch * l_end bytes, contiguous NCHW of layer end_idx.  Chunked by max_batch like the
+ * prefix.  Errors: INVALID_ARGUMENT (not a suffix model, end_idx out of range, null, batch 0),
+ * CUDA. */
+HAPI_API hapi_status hapi_suffix_forward(hapi_model *m, uint32_t end_idx, const void *acts, uint64_t batch,
+                                         void *out);
+
 /* End-to-end variant with HOST buffers (pinned or pageable): images [batch,3,H,W] fp32
  * host -> device copies, prefix forward, device -> host copy of the split output into
  * host `out`, pipelined in max_batch chunks over two streams (H2D of chunk i+1 overlaps

@@ -37,3 +37,14 @@ def prefix_forward_all(arch: str, params, images: np.ndarray, upto: int | None =
         x = m.fwd(x, params)
         outs.append(x)
     return outs
+
+
+def suffix_forward(arch: str, params, acts: np.ndarray, start_idx: int, end_idx: int) -> np.ndarray:
+    """Layers start_idx+1 .. end_idx applied to layer start_idx's output (the client-side
+    frozen suffix, PAPER.md:734 / SURVEY 8(f) f3): the same per-layer definitions, begun
+    later.  acts: [B, C, H, W] (or [B, F]) as layer start_idx produces it."""
+    mods = archs.layers(arch)
+    x = np.asarray(acts, dtype=np.float64)
+    for m in mods[start_idx:end_idx]:
+        x = m.fwd(x, params)
+    return x

@@ -114,7 +114,9 @@ class Model:
     torch tensors) in hapi_param_table order."""
 
     def __init__(self, arch, act, params: Sequence, max_batch: int, min_split: int, max_split: Optional[int] = None,
-                 in_h: int = 224, in_w: int = 224, device: int = 0):
+                 in_h: int = 224, in_w: int = 224, device: int = 0, start_idx: int = 0):
+        """start_idx > 0: a client-side suffix model (input = layer start_idx's NCHW output,
+        computes layers start_idx+1 .. split; use forward_suffix)."""
         import numpy as np
         max_split = min_split if max_split is None else max_split
         self.arch, self.act = arch, act
@@ -124,7 +126,11 @@ class Model:
         ptrs = (C.c_void_p * len(keep))(*[p.ctypes.data for p in keep])
         d = _lib.ModelDesc(_arch(arch), _dt(act), in_h, in_w, min_split, max_split, max_batch, device)
         h = C.c_void_p()
-        _check(_lib.hapi_model_create(C.byref(d), ptrs, len(keep), C.byref(h)))
+        if start_idx:
+            _check(_lib.hapi_model_create_suffix(C.byref(d), start_idx, ptrs, len(keep), C.byref(h)))
+        else:
+            _check(_lib.hapi_model_create(C.byref(d), ptrs, len(keep), C.byref(h)))
+        self.start_idx = start_idx
         self._h = h
         self.device = device
         self.out_bytes = hapi_layer_sizes(arch, in_h, in_w, act)[1]
@@ -148,6 +154,14 @@ class Model:
         for the split output (act dtype).  Launches on the model's stream."""
         assert images.is_cuda and images.is_contiguous() and out.is_cuda and out.is_contiguous()
         _check(_lib.hapi_prefix_forward(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
+                                        C.c_void_p(out.data_ptr())))
+        return out
+
+    def forward_suffix(self, end_idx: int, acts, out):
+        """acts: CUDA tensor holding layer start_idx's output (NCHW, act dtype); out: CUDA
+        tensor with room for layer end_idx's output."""
+        assert acts.is_cuda and acts.is_contiguous() and out.is_cuda and out.is_contiguous()
+        _check(_lib.hapi_suffix_forward(self._h, end_idx, C.c_void_p(acts.data_ptr()), acts.shape[0],
                                         C.c_void_p(out.data_ptr())))
         return out
 

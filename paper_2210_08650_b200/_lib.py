@@ -55,6 +55,9 @@ hapi_num_params = _sig("hapi_num_params", i32, C.c_int)
 hapi_param_info = _sig("hapi_param_info", C.c_int, C.c_int, u32, C.c_char_p, u32, C.POINTER(i64), P_u32)
 hapi_model_create = _sig("hapi_model_create", C.c_int, C.POINTER(ModelDesc), C.POINTER(C.c_void_p), u32,
                          C.POINTER(C.c_void_p))
+hapi_model_create_suffix = _sig("hapi_model_create_suffix", C.c_int, C.POINTER(ModelDesc), u32, C.POINTER(C.c_void_p),
+                                u32, C.POINTER(C.c_void_p))
+hapi_suffix_forward = _sig("hapi_suffix_forward", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
 hapi_model_set_stream = _sig("hapi_model_set_stream", C.c_int, C.c_void_p, C.c_void_p)
 hapi_prefix_forward = _sig("hapi_prefix_forward", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
 hapi_prefix_forward_host = _sig("hapi_prefix_forward_host", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
@@ -68,7 +71,7 @@ hapi_last_error = _sig("hapi_last_error", C.c_char_p)
 hapi_build_info = _sig("hapi_build_info", C.c_char_p)
 
 EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_choose_split", "hapi_adapt_batches",
-            "hapi_partition_requests", "hapi_num_params",
+            "hapi_partition_requests", "hapi_model_create_suffix", "hapi_suffix_forward", "hapi_num_params",
             "hapi_param_info", "hapi_model_create", "hapi_model_set_stream", "hapi_prefix_forward",
             "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_plan_describe", "hapi_prefix_forward_timed",
             "hapi_model_destroy", "hapi_last_error", "hapi_build_info"]

@@ -136,6 +136,8 @@ int conv_simt_ksplit(long long M, int Cout, int K, int num_sms);
 // [N][H/2+3][W/2+3][16]; padded pixel (i+2, j+2) channel (a*2+b)*3+c holds image pixel
 // (2i+a, 2j+b) channel c; channels 12..15 and the border are zero.
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st);
+// Contiguous NCHW [N][C][HW] (act dtype, es = 2 or 4 bytes) -> NHWC with pixel stride y_ld.
+cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int y_ld, int es, cudaStream_t st);
 
 // Window pooling, NHWC -> NHWC.  mode 0 = max (-inf padding), 1 = avg (count k*k).
 struct PoolArgs {

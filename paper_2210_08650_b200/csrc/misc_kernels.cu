@@ -236,6 +236,29 @@ __global__ void pack_output_kernel(const T* __restrict__ x, int HW, int C, int x
   }
 }
 
+// NCHW [N][C][HW] -> NHWC [N*HW][y_ld] (the suffix path's input: the split-layer send
+// buffer of the storage side becomes the client's first activation)
+template <typename T>
+__global__ void unpack_nchw_kernel(const T* __restrict__ x, int HW, int C, T* __restrict__ y, int y_ld) {
+  griddep_launch_dependents();
+  griddep_wait();
+  __shared__ T tile[32][33];
+  const int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
+  const long long n = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + ty + 8 * i, p = p0 + tx;
+    if (p < HW && c < C) tile[ty + 8 * i][tx] = x[(n * C + c) * HW + p];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int p = p0 + ty + 8 * i, c = c0 + tx;
+    if (p < HW && c < C) y[(n * HW + p) * y_ld + c] = tile[tx][ty + 8 * i];
+  }
+}
+
 inline int grid_for(long long total, int block) {
   long long g = (total + block - 1) / block;
   if (g > 148 * 32) g = 148 * 32;
@@ -245,6 +268,18 @@ inline int grid_for(long long total, int block) {
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
+
+cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int y_ld, int es, cudaStream_t st) {
+  if (N <= 0 || C <= 0 || HW <= 0) return cudaSuccess;
+  dim3 grid((C + 31) / 32, (HW + 31) / 32, N), block(32, 8);
+  if (es == 2)
+    launch_pdl(unpack_nchw_kernel<__nv_bfloat16>, grid, block, 0, st, static_cast<const __nv_bfloat16*>(x), HW, C,
+               static_cast<__nv_bfloat16*>(y), y_ld);
+  else
+    launch_pdl(unpack_nchw_kernel<float>, grid, block, 0, st, static_cast<const float*>(x), HW, C,
+               static_cast<float*>(y), y_ld);
+  return cudaGetLastError();
+}
 
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st) {
   const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * (W / 2 + 3) : (long long)N * H * W;

@@ -154,7 +154,7 @@ struct ConvW {
   bool res_identity = false;         // K2 columns are an identity block: + residual inside the GEMM
 };
 
-enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT, OP_PAIR };
+enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT, OP_PAIR, OP_UNPACK };
 
 struct View {
   int buf = -1;       // -1: external (caller out, or caller images for PACK_IN input)
@@ -222,6 +222,8 @@ struct hapi_model {
   std::vector<const float*> host_params;  // valid during create only
   std::vector<void*> allocs;
   int64_t weight_bytes = 0;
+  uint32_t start = 0;                          // suffix models: input = layer `start` output
+  int64_t in_bytes_per_img = 0;                // suffix models: bytes of one input activation
   void* ident = nullptr;                       // shared 256x256 bf16 identity (residual in GEMM)
   CUtensorMap ident_map128, ident_map256;      // box {64, 128} / {64, 256}
   std::vector<Plan> plans;  // index split - min_split
@@ -635,11 +637,13 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   // 2x2 space-to-depth layout (16 channels at H/2 x W/2) so the stem gathers 16-byte pieces;
   // other stems read the image padded to 8 channels.
   const ModDesc& m0 = A.mods[0];
-  const bool s2d = m->bf16 && m0.kind == MK_CONV && m0.k == 7 && m0.stride == 2 && m0.pad == 3 && m0.cin == 3 &&
-                   H0 % 2 == 0 && W0 % 2 == 0;
+  const int start = (int)m->start;
+  const bool s2d = start == 0 && m->bf16 && m0.kind == MK_CONV && m0.k == 7 && m0.stride == 2 && m0.pad == 3 &&
+                   m0.cin == 3 && H0 % 2 == 0 && W0 % 2 == 0;
   const int layout = !m->bf16 ? 0 : (s2d ? 2 : 1);
-  View cur = layout == 2 ? b.compact(16, H0 / 2 + 3, W0 / 2 + 3) : b.compact(layout == 1 ? 8 : 3, H0, W0);
-  {
+  View cur;
+  if (start == 0) {
+    cur = layout == 2 ? b.compact(16, H0 / 2 + 3, W0 / 2 + 3) : b.compact(layout == 1 ? 8 : 3, H0, W0);
     Op o;
     o.t = OP_PACK_IN;
     o.out = cur;
@@ -647,9 +651,26 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     o.layout = layout;
     o.bytes = (double)H0 * W0 * 3 * 4 + (double)cur.C * cur.H * cur.W * m->es;
     b.emit(o);
+  } else {
+    // suffix plan: the input is layer `start`'s output in the send-buffer
+    // layout (contiguous NCHW, act dtype) -- unpacked to NHWC, then layers start+1..split
+    Shape sh{3, H0, W0, false};
+    for (int k = 0; k < start; ++k) {
+      bool ok;
+      sh = infer(A.mods[k], sh, &ok);
+      if (!ok) return set_error(HAPI_ERR_INVALID_MODEL, "layer %s empty", A.mods[k].name.c_str());
+    }
+    cur = sh.flat ? b.compact(sh.c, 1, 1) : b.compact(sh.c, sh.h, sh.w);
+    Op o;
+    o.t = OP_UNPACK;
+    o.out = cur;
+    o.kind = 3;
+    o.bytes = 2.0 * (double)cur.C * cur.H * cur.W * m->es;
+    o.desc = "unpack layer " + std::to_string(start) + " (NCHW -> NHWC)";
+    b.emit(o);
   }
   const auto& mods = A.mods;
-  int i = 0;
+  int i = start;
   hapi_status st;
   while (i < split) {
     const ModDesc& md = mods[i];
@@ -1055,6 +1076,9 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
     case OP_PACK_IN:
       e = pack_input_launch(images, vptr(m, p, o.out, out), nb, (int)m->d.in_h, (int)m->d.in_w, o.layout, st);
       break;
+    case OP_UNPACK:
+      e = unpack_nchw_launch(images, nb, o.out.C, o.out.H * o.out.W, vptr(m, p, o.out, out), o.out.ld, m->es, st);
+      break;
     case OP_PAIR: {
       const ConvW& wa = m->convs[o.conv];
       const ConvW& wb = m->convs[o.conv2];
@@ -1395,7 +1419,24 @@ const Plan* get_plan(hapi_model* m, uint32_t split) {
 
 extern "C" {
 
+static hapi_status create_impl(const hapi_model_desc* desc, uint32_t start, const float* const* params,
+                               uint32_t n_params, hapi_model** out);
+
 hapi_status hapi_model_create(const hapi_model_desc* desc, const float* const* params, uint32_t n_params, hapi_model** out) {
+  return create_impl(desc, 0, params, n_params, out);
+}
+
+hapi_status hapi_model_create_suffix(const hapi_model_desc* desc, uint32_t start_idx, const float* const* params,
+                                     uint32_t n_params, hapi_model** out) {
+  clear_error();
+  if (!desc) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null desc");
+  if (start_idx < 1 || start_idx >= desc->min_split)
+    return set_error(HAPI_ERR_INVALID_ARGUMENT, "start_idx %u must be in [1, min_split)", start_idx);
+  return create_impl(desc, start_idx, params, n_params, out);
+}
+
+static hapi_status create_impl(const hapi_model_desc* desc, uint32_t start, const float* const* params,
+                               uint32_t n_params, hapi_model** out) {
   clear_error();
   if (!desc || !out || (!params && n_params)) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
@@ -1411,12 +1452,14 @@ hapi_status hapi_model_create(const hapi_model_desc* desc, const float* const* p
   for (uint32_t k = 0; k < n_params; ++k)
     if (!params[k]) return set_error(HAPI_ERR_INVALID_ARGUMENT, "params[%u] is null", k);
   // shape validity at this image size
+  int64_t in_numel = 3ll * desc->in_h * desc->in_w;
   {
     Shape s{3, (int)desc->in_h, (int)desc->in_w, false};
     for (uint32_t k = 0; k < desc->max_split; ++k) {
       bool ok;
       s = infer(A->mods[k], s, &ok);
       if (!ok) return set_error(HAPI_ERR_INVALID_MODEL, "layer %s empty at %ux%u", A->mods[k].name.c_str(), desc->in_h, desc->in_w);
+      if (k + 1 == start) in_numel = s.numel();
     }
   }
   HAPI_CUDA_TRY(cudaSetDevice(desc->device));
@@ -1425,6 +1468,8 @@ hapi_status hapi_model_create(const hapi_model_desc* desc, const float* const* p
   m->arch = A;
   m->bf16 = desc->act == HAPI_BF16;
   m->es = m->bf16 ? 2 : 4;
+  m->start = start;
+  m->in_bytes_per_img = start ? in_numel * m->es : in_numel * 4;
   HAPI_CUDA_TRY(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, desc->device));
   if (m->bf16) {
     int major = 0, minor = 0;
@@ -1468,9 +1513,29 @@ hapi_status hapi_model_set_stream(hapi_model* m, void* s) {
   return HAPI_OK;
 }
 
+hapi_status hapi_suffix_forward(hapi_model* m, uint32_t end_idx, const void* acts, uint64_t batch, void* out) {
+  clear_error();
+  if (!m || !acts || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (m->start == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "not a suffix model (use hapi_prefix_forward)");
+  if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
+  const Plan* p = get_plan(m, end_idx);
+  if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "end_idx %u outside [%u,%u]", end_idx, m->d.min_split, m->d.max_split);
+  HAPI_CUDA_TRY(cudaGetLastError());
+  const bool use_graph = (batch + m->d.max_batch - 1) / m->d.max_batch <= 4;
+  for (uint64_t c0 = 0; c0 < batch; c0 += m->d.max_batch) {
+    const int nb = (int)std::min<uint64_t>(m->d.max_batch, batch - c0);
+    const float* ci = reinterpret_cast<const float*>(static_cast<const char*>(acts) + c0 * m->in_bytes_per_img);
+    void* co = static_cast<char*>(out) + c0 * p->out_bytes_per_img;
+    hapi_status st = use_graph ? run_chunk_graph(m, *p, nb, ci, co) : run_chunk(m, *p, nb, ci, co, m->stream);
+    if (st != HAPI_OK) return st;
+  }
+  return HAPI_OK;
+}
+
 hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
   if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
@@ -1493,6 +1558,7 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
                                       float* ms, uint32_t cap) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
   if (batch == 0 || batch > m->d.max_batch) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch must be in [1, max_batch]");
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
@@ -1512,6 +1578,7 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
 hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
   if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
@@ -1575,7 +1642,7 @@ hapi_status hapi_plan_describe(const hapi_model* m, uint32_t split_idx, uint32_t
   if (split_idx < m->d.min_split || split_idx > m->d.max_split) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx");
   const Plan& p = m->plans[split_idx - m->d.min_split];
   if (op >= p.ops.size()) return set_error(HAPI_ERR_INVALID_ARGUMENT, "op index");
-  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out", "pair"};
+  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out", "pair", "unpack"};
   const Op& o = p.ops[op];
   std::snprintf(buf, cap, "%s%s%s", o.desc.empty() ? names[o.t] : o.desc.c_str(), o.out.buf < 0 ? " ->out" : "",
                 o.nchw_out ? "(nchw)" : "");
