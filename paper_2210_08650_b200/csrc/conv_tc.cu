@@ -901,11 +901,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (m < 0 || n0 >= a.Cout) continue;
           __nv_bfloat16* yp = yb + ((long long)img * a.Cout + n0) * OHW + pix;
           const __nv_bfloat16* rp = rb ? rb + m * a.res_ld + n0 : nullptr;
+          // residual: the thread's 32 channels as four 16-byte loads (not 32 scalar loads)
+          float res[32];
+          const bool full32 = n0 + 32 <= a.Cout;
+          if (rp && full32 && (a.res_ld % 8) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = __ldg(reinterpret_cast<const uint4*>(rp) + q);
+              const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const float2 f2 = unpack_bf16x2(uu[h]);
+                res[q * 8 + 2 * h] = f2.x;
+                res[q * 8 + 2 * h + 1] = f2.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) res[j] = (rp && n0 + j < a.Cout) ? __bfloat162float(rp[j]) : 0.f;
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (n0 + j < a.Cout) {
-              float f = __uint_as_float(v[j]) + sBias[j0 + j];
-              if (rp) f += __bfloat162float(rp[j]);
+              float f = __uint_as_float(v[j]) + sBias[j0 + j] + res[j];
               if (a.relu) f = fmaxf(f, 0.f);
               yp[(long long)j * OHW] = __float2bfloat16_rn(f);
             }
