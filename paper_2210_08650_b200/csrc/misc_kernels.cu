@@ -259,6 +259,38 @@ __global__ void unpack_nchw_kernel(const T* __restrict__ x, int HW, int C, T* __
   }
 }
 
+// bf16 NHWC -> NCHW with 16-byte accesses on both sides: a 64-pixel x 64-channel tile is read
+// as 8-channel vectors along C and written as 8-pixel vectors along HW (HW % 8 == 0, C % 8 == 0)
+__global__ void __launch_bounds__(256) pack_output_v8_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C,
+                                                             int x_ld, __nv_bfloat16* __restrict__ y) {
+  griddep_launch_dependents();
+  griddep_wait();
+  __shared__ __align__(16) __nv_bfloat16 tile[64][64 + 8];  // [channel][pixel], padded rows
+  const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  const long long n = blockIdx.z;
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int idx = t + k * 256;              // 64 pixels x 8 channel-chunks
+    const int pp = idx >> 3, cc = (idx & 7) * 8;
+    const int p = p0 + pp, c = c0 + cc;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (p < HW && c < C) v = __ldg(reinterpret_cast<const uint4*>(x + (n * HW + p) * x_ld + c));
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) tile[cc + j][pp] = e[j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int idx = t + k * 256;              // 64 channels x 8 pixel-chunks
+    const int cc = idx >> 3, pp = (idx & 7) * 8;
+    const int c = c0 + cc, p = p0 + pp;
+    if (c < C && p < HW)
+      *reinterpret_cast<uint4*>(y + (n * C + c) * HW + p) = *reinterpret_cast<const uint4*>(&tile[cc][pp]);
+  }
+}
+
 inline int grid_for(long long total, int block) {
   long long g = (total + block - 1) / block;
   if (g > 148 * 32) g = 148 * 32;
@@ -339,6 +371,11 @@ cudaError_t pack_output_launch(const void* x, int N, int HW, int C, int x_ld, vo
   const size_t es = is_bf16 ? 2 : 4;
   if (HW == 1) {  // NHWC == NCHW: a strided row copy
     return cudaMemcpy2DAsync(y, C * es, x, (size_t)x_ld * es, C * es, N, cudaMemcpyDeviceToDevice, st);
+  }
+  if (is_bf16 && HW % 8 == 0 && C % 8 == 0 && x_ld % 8 == 0 && aligned16(x) && aligned16(y)) {
+    launch_pdl(pack_output_v8_kernel, dim3((HW + 63) / 64, (C + 63) / 64, N), dim3(256), 0, st,
+               static_cast<const __nv_bfloat16*>(x), HW, C, x_ld, static_cast<__nv_bfloat16*>(y));
+    return cudaGetLastError();
   }
   dim3 grid((HW + 31) / 32, (C + 31) / 32, N), block(32, 8);
   if (is_bf16)
