@@ -52,7 +52,8 @@ constexpr int XFORM_TMA_WARP = 14;   // mode 7: TMA issuer while warps 8-11 tran
 constexpr int NUM_THREADS = 15 * 32;
 constexpr int M8_POOL_WARP0 = 9;      // mode 8: warps 9-11 pool while 0-7 drain TMEM
 constexpr int M8_POOL_THREADS = 96;
-constexpr int M8_RING = 6;            // mode 8: stem rows held in smem (tile i: rows 2i, 2i+1)
+constexpr int M8_ROWS = 5;            // mode 8: padded s2d rows per tile (2 stem rows + 3 taps)
+constexpr int M8_CHUNKS = M8_ROWS * 4; // mode 8: K chunks (s2d row x tap column), K = 16 each
 constexpr int A_STAGE_BYTES = BM * BK * 2;
 constexpr int SMEM_LIMIT = 232448;                           // 227 KB opt-in per CTA
 constexpr int MAX_STAGES = 8;
@@ -97,7 +98,7 @@ struct Geo {
   int cps;                     // K chunks per pipeline stage (modes 3/4: 2 when BN <= 128)
   int pro_c;                   // mode 7: channels of the smem scale/shift tables (C rounded to 64)
   int ph, pw, pq, strips, n_tasks;  // mode 8: pooled map, pool columns per strip, strips/image, tasks
-  int ring_bytes;                   // mode 8: M8_RING stem rows x (2 pq + 1) pixels x 128 B
+  int ring_bytes;                   // mode 8: two [2 we x 128 B] buffers of vertically pooled rows
   int res_depth;                    // residual ring depth (blocks of [128 x SB] in flight)
   int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
   int mc;                           // 1: 2-CTA cluster, each weight chunk multicast to both CTAs
@@ -129,8 +130,8 @@ __device__ __forceinline__ long long row_to_m(const ConvArgs& a, const Geo& g, i
   return ((long long)n * a.OH + oh) * a.OW + ow;
 }
 
-// k-th tile of this CTA (-1 when done).  Mode 8 hands out whole (image, strip) tasks so a
-// CTA walks one strip's pooled rows in order (the previous stem row stays in smem).
+// k-th tile of this CTA (-1 when done).  Mode 8 hands out whole (image, strip pair) tasks so a
+// CTA walks one task's pooled rows in order (the previous stem row stays in registers).
 __device__ __forceinline__ int tile_at(const Geo& g, int k, int num_tiles) {
   if (g.mode == 8) {
     const int task = blockIdx.x + (k / g.ph) * gridDim.x;
@@ -150,10 +151,10 @@ __device__ __forceinline__ int tile_at(const Geo& g, int k, int num_tiles) {
 
 // Spatial origin of m-tile tm in mode 4 (output coordinates).
 __device__ __forceinline__ void tile_origin(const Geo& g, int tm, int* w0, int* h0, int* b0) {
-  if (g.mode == 8) {  // stem rows 2po, 2po+1, stem columns from 2 q0 - 1 (pool padding)
+  if (g.mode == 8) {  // (image, strip pair, pooled row): strip coordinate 2p, s2d rows from 2po
     const int po = tm % g.ph, task = tm / g.ph;
-    *b0 = task / g.strips;
-    *w0 = 2 * (task % g.strips) * g.pq - 1;
+    *b0 = task / g.strips;            // g.strips = strip pairs per image in mode 8
+    *w0 = 2 * (task % g.strips);
     *h0 = 2 * po;
     return;
   }
@@ -331,103 +332,110 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (MODE == 8 && warp >= M8_POOL_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ mode 8 pooling
-    // 3x3/s2/p1 max over the ring: pooled row po of a strip = max over stem rows 2po-1..2po+1
-    // (ring rows 2i-1, 2i, 2i+1 of local tile i; at po = 0 row 2i stands in for the missing
-    // row -1 -- values are >= 0 after ReLU and max is idempotent).  Item = (pooled column,
-    // 8-channel group); 16-byte swizzled smem reads, one 16-byte global store.
+    // Horizontal half of the 3x3/s2/p1 max: the epilogue already took the vertical max over
+    // stem rows 2po-1..2po+1 into V (one row per strip column); pooled column q of strip k =
+    // max(V[2qo], V[2qo+1], V[2qo+2]).  Item = (strip, pooled column, 8-channel group): three
+    // swizzled 16-byte smem reads, one 16-byte global store.
     const int pt = threadIdx.x - M8_POOL_WARP0 * 32;
-    const int rowbytes = (2 * g.pq + 1) * 128;
-    const uint32_t ring = smem_u32(sY);
     __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.y);
-    int po = 0, task = blockIdx.x, img = task / g.strips, q0 = (task - img * g.strips) * g.pq, kslot = 0;
+    const int items = 2 * g.pq * 8;
+    int po = 0, task = blockIdx.x;
     for (int it = 0; task < g.n_tasks; ++it) {
+      const int img = task / g.strips, pair = task - img * g.strips;
       mbar_wait(&pready[it & 1], (it >> 1) & 1);
-      const int r0 = 2 * kslot, r1 = r0 + 1, rp = po == 0 ? r0 : (r0 == 0 ? M8_RING - 1 : r0 - 1);
-      const uint32_t b0 = ring + rp * rowbytes, b1 = ring + r0 * rowbytes, b2 = ring + r1 * rowbytes;
-      for (int item = pt; item < g.pq * 8; item += M8_POOL_THREADS) {
-        const int qo = item >> 3, cg = item & 7;
-        if (q0 + qo >= g.pw) continue;
+      const uint32_t vbuf = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2));
+      for (int item = pt; item < items; item += M8_POOL_THREADS) {
+        const int k = item / (g.pq * 8), rem = item - k * (g.pq * 8);
+        const int qo = rem >> 3, cg = rem & 7;
+        const int q = (2 * pair + k) * g.pq + qo;
+        if (qo >= g.pq || q >= g.pw) continue;
         uint32_t mx[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int dc = 0; dc < 3; ++dc) {
-          const int col = 2 * qo + dc;
-          const uint32_t off = (uint32_t)(col * 128 + ((cg ^ (col & 7)) << 4));
-          const uint32_t rb[3] = {b0, b1, b2};
+          const int x = 2 * qo + dc;
+          const uint32_t addr = vbuf + (uint32_t)((k * g.we + x) * 128 + ((cg ^ (x & 7)) << 4));
+          uint32_t u[4];
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                       : "r"(addr));
 #pragma unroll
-          for (int dr = 0; dr < 3; ++dr) {
-            uint32_t u[4];
-            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
-                         : "r"(rb[dr] + off));
-#pragma unroll
-            for (int j = 0; j < 4; ++j) mx[j] = bf16x2_max(mx[j], u[j]);
-          }
+          for (int j = 0; j < 4; ++j) mx[j] = bf16x2_max(mx[j], u[j]);
         }
-        *reinterpret_cast<uint4*>(yb + (((long long)img * g.ph + po) * g.pw + q0 + qo) * a.y_ld + cg * 8) =
+        *reinterpret_cast<uint4*>(yb + (((long long)img * g.ph + po) * g.pw + q) * a.y_ld + cg * 8) =
             make_uint4(mx[0], mx[1], mx[2], mx[3]);
       }
       mbar_arrive(&pfree[it & 1]);
-      kslot = kslot == M8_RING / 2 - 1 ? 0 : kslot + 1;
       if (++po == g.ph) {
         po = 0;
         task += gridDim.x;
-        img = task / g.strips;
-        q0 = (task - img * g.strips) * g.pq;
       }
     }
   } else if (MODE == 8 && warp < NUM_EPI_WARPS) {
     // ================================================================ mode 8 epilogue
-    // TMEM -> + bias (registers) -> ReLU -> bf16 -> the two stem rows of the tile into ring
-    // rows 2i, 2i+1 (swizzled 16-byte chunks), then signal the pooling warps.  Runs one tile
-    // ahead of the pooling: tile i reuses the ring rows of tile i-3, pooled by tile i-2 at
-    // the latest (pfree).
+    // TMEM lane = strip column (strip k = row / we, column x = row % we); accumulator columns
+    // 0-63 = stem row 2po, 64-127 = stem row 2po+1 (the MMA's N covers both rows).  Each thread
+    // holds 32 channels of both rows, relu(+bias) in fp32, and keeps row 2po+1 in registers for
+    // the next pooled row: V = max(row 2po-1, row 2po, row 2po+1) is the vertical pool, written
+    // once to smem for the pooling warps (ReLU >= 0, so padding is 0; max commutes with the
+    // bf16 rounding, so V equals pooling the rounded stem map).
     const int quarter = warp & 3, gsel = warp >> 2;
     const int row = quarter * 32 + lane;
-    const int sr = row / g.we, sc = row - sr * g.we;
-    const bool live = sr < 2 && sc < 2 * g.pq + 1;
-    const int rowbytes = (2 * g.pq + 1) * 128;
-    const uint32_t ring = smem_u32(sY) + (uint32_t)(sr * rowbytes + sc * 128);
-    float bias[32];
+    const int k = row / g.we, x = row - (row / g.we) * g.we;
+    const bool live = k < 2 && x < 2 * g.pq + 1;
+    float bias[32], prev[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int n = gsel * 32 + j;
       bias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
+      prev[j] = 0.f;
     }
-    int po = 0, task = blockIdx.x, q0 = (task % g.strips) * g.pq, kslot = 0;
+    int po = 0, task = blockIdx.x;
     for (int it = 0; task < g.n_tasks; ++it) {
       const int acc = it & 1;
+      const int pair = task % g.strips;
+      const int stem_col = 2 * (2 * pair + k) * g.pq - 1 + x;
+      const bool valid = live && stem_col >= 0 && stem_col < a.OW;
+      const bool valid1 = valid && 2 * po + 1 < a.OH;
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
-      mbar_wait(&pfree[it & 1], ((it >> 1) & 1) ^ 1);
-      const int stem_row = 2 * po + sr, stem_col = 2 * q0 - 1 + sc;
-      const bool valid = live && stem_col >= 0 && stem_col < a.OW && stem_row < a.OH;
-      uint32_t v[32];
-      tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + gsel * 32, v);
+      uint32_t v0[32], v1[32];
+      const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + gsel * 32;
+      tmem_ld32(tb, v0);
+      tmem_ld32(tb + 64, v1);
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      mbar_wait(&pfree[it & 1], ((it >> 1) & 1) ^ 1);
       if (live) {
-        const uint32_t dst = ring + (uint32_t)(2 * kslot * rowbytes);
+        const uint32_t dst = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2) + row * 128);
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
-          uint32_t o[4] = {0u, 0u, 0u, 0u};
-          if (valid) {
+          uint32_t o[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              o[j] = cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * j]) + bias[c4 * 8 + 2 * j],
-                                     __uint_as_float(v[c4 * 8 + 2 * j + 1]) + bias[c4 * 8 + 2 * j + 1]);
+          for (int j = 0; j < 4; ++j) {
+            float f[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int c = c4 * 8 + 2 * j + h;
+              const float r0 = valid ? fmaxf(__uint_as_float(v0[c]) + bias[c], 0.f) : 0.f;
+              const float r1 = valid1 ? fmaxf(__uint_as_float(v1[c]) + bias[c], 0.f) : 0.f;
+              f[h] = fmaxf(fmaxf(prev[c], r0), r1);
+              prev[c] = r1;
+            }
+            o[j] = pack_bf16x2(f[0], f[1]);
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (((gsel * 4 + c4) ^ (sc & 7)) << 4)),
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (((gsel * 4 + c4) ^ (x & 7)) << 4)),
                        "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
         }
       }
+      fence_proxy_async_smem();
       mbar_arrive(&pready[it & 1]);
-      kslot = kslot == M8_RING / 2 - 1 ? 0 : kslot + 1;
       if (++po == g.ph) {
         po = 0;
         task += gridDim.x;
-        q0 = (task % g.strips) * g.pq;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) prev[j] = 0.f;  // a new (image, strip pair): row -1 is padding
       }
     }
   } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
@@ -447,18 +455,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       __syncwarp();
     }
     if (MODE == 8) {
-      // stem halo: resident weights once, then per tile one [5 rows x we] box of the padded
-      // s2d input as two 16-byte-per-pixel planes (channels 0-7 | 8-15).  (A single
-      // 32-byte-swizzled box read through SW32 descriptors is correct too but measured
-      // slower: 0.43 vs 0.37 ms for ResNet-50 b512.)
+      // stem: resident weights (20 K chunks x [2 k-halves][128 n][8], 80 KB) once, then per
+      // tile one 5D box {8 ch, we cols, 2 strips, 5 s2d rows, 1} per 8-channel plane: smem
+      // [row][strip][col] x 16 B, so each (row, tap column) K chunk is a row-shifted view
       if (warp == PROD_WARP0) {
         if (elect_one()) {
-          mbar_arrive_expect_tx(bres, 16 * 2 * 64 * 16);
-          bulk_load_1d(smem_u32(sB), a.w, 16 * 2 * 64 * 16, bres);
+          mbar_arrive_expect_tx(bres, M8_CHUNKS * 4096);
+          bulk_load_1d(smem_u32(sB), a.w, M8_CHUNKS * 4096, bres);
         }
         __syncwarp();
         uint32_t ast = 0, aph = 0;
-        const uint32_t plane_stride = ((uint32_t)g.a_bytes / 2 + 127) / 128 * 128;
+        const uint32_t plane_stride = (uint32_t)g.a_stage_bytes / 2;
         for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
           int w0, h0, b0;
           tile_origin(g, tile, &w0, &h0, &b0);
@@ -466,8 +473,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (elect_one()) {
             mbar_arrive_expect_tx(&afull[ast], g.a_bytes);
             const uint32_t dst = smem_u32(sA + ast * ASZ);
-            tma_load_4d(dst, &tmap_a, 0, w0, h0, b0, &afull[ast]);
-            tma_load_4d(dst + plane_stride, &tmap_a, 8, w0, h0, b0, &afull[ast]);
+            tma_load_5d(dst, &tmap_a, 0, 0, w0, h0, b0, &afull[ast]);
+            tma_load_5d(dst + plane_stride, &tmap_a, 8, 0, w0, h0, b0, &afull[ast]);
           }
           __syncwarp();
           if (++ast == (uint32_t)AS) { ast = 0; aph ^= 1; }
@@ -699,20 +706,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         if (MODE == 8) {
-          // 16 taps (r, s) of the 4x4 s2d stem, K = 16 each: A = the halo planes shifted by
-          // r*we + s pixels (16 B per pixel per plane), B = resident [tap][k half][n][8].
-          // N = 64 MMAs are smem-bandwidth bound (48 cycles measured vs 32 floor:
-          // tools/micro/mma_rate.cu), and the epilogue/pooling smem traffic shares that port.
-          const uint32_t plane_stride = ((uint32_t)g.a_bytes / 2 + 127) / 128 * 128;
+          // 20 K chunks (s2d row rho, tap column s), K = 16 each, N = 128 = both stem rows of
+          // the tile (row 2po uses tap row rho, row 2po+1 tap row rho-1; the weight block holds
+          // zeros where a tap does not apply).  A = the box planes of row rho shifted by s
+          // columns; M rows = [strip 0 columns | strip 1 columns].  N = 128 runs the tensor
+          // core at full rate where two N = 64 tiles were smem-bound (tools/micro/mma_rate.cu).
+          const uint32_t plane_stride = (uint32_t)g.a_stage_bytes / 2;
+          const uint32_t row_stride = (uint32_t)(2 * g.we * 16);
           mbar_wait(&afull[ast], aph);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a_base = sA0 + ast * ASZ;
 #pragma unroll 1
-            for (int t = 0; t < 16; ++t) {
-              const int r = t >> 2, sft = t & 3;
-              const uint64_t adesc = make_sdesc_none(a_base + (uint32_t)(r * g.we + sft) * 16u, plane_stride, 128);
-              const uint64_t bdesc = make_sdesc_none(sB0 + t * 2048, 1024, 128);
+            for (int t = 0; t < M8_CHUNKS; ++t) {
+              const int rho = t >> 2, sft = t & 3;
+              const uint64_t adesc = make_sdesc_none(a_base + rho * row_stride + (uint32_t)sft * 16u, plane_stride, 128);
+              const uint64_t bdesc = make_sdesc_none(sB0 + t * 4096, 2048, 128);
               mma_bf16(d_tmem, adesc, bdesc, idesc, t != 0);
             }
             mma_commit(&aempty[ast]);
@@ -1080,6 +1089,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   if (g.mode == 8) {
     g.b_res = 1;
     g.stages = 2;  // B ring unused (placeholder for the barrier init loop)
+    if (2 * g.we > BM) return cudaErrorInvalidValue;
     const int ring_extra = g.ring_bytes > 2 * C::SB_BYTES ? g.ring_bytes - 2 * C::SB_BYTES : 0;
     smem = g.a_stages * g.a_stage_bytes + bres_bytes + C::FIXED + ring_extra;
     if (smem > SMEM_LIMIT) return cudaErrorInvalidValue;
@@ -1156,7 +1166,7 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
       return launch_t<BN, 6>(a, g, mp, num_sms, st);
     case 7: return launch_t<BN, 7>(a, g, mp, num_sms, st);
     case 8:
-      if constexpr (BN == 64) return launch_t<BN, 8>(a, g, mp, num_sms, st);
+      if constexpr (BN == 128) return launch_t<BN, 8>(a, g, mp, num_sms, st);
       return cudaErrorInvalidValue;
   }
   return cudaErrorInvalidValue;
@@ -1205,29 +1215,31 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   g.has_res = a.res != nullptr;
   g.tma_out = !a.nchw;
   if (mode == 8) {
-    // stem conv (window view, KH=4 x 64 channels) fused with the 3x3/s2/p1 maxpool: a tile is
-    // 2 stem rows x (2 pq + 1) stem columns of one image strip; tasks = images x strips
-    if (a.Cout > 64 || a.C != BK || a.stride != 1) return cudaErrorInvalidValue;
+    // stem conv fused with the 3x3/s2/p1 maxpool: a tile is one pooled row of a pair of
+    // strips of pq pooled columns (2 pq + 1 stem columns + 3 tap columns = we box columns per
+    // strip); tasks = images x strip pairs, each walked row by row by one CTA
+    if (a.Cout > 64 || a.C != BK || a.stride != 1 || bn != 128) return cudaErrorInvalidValue;
     g.pw = (a.OW - 1) / 2 + 1;
     g.ph = (a.OH - 1) / 2 + 1;
-    g.strips = (g.pw + 30) / 31;
-    g.pq = (g.pw + g.strips - 1) / g.strips;
+    const int S = (g.pw + 29) / 30;
+    g.pq = (g.pw + S - 1) / S;
+    g.strips = (S + 1) / 2;                    // strip pairs
     g.n_tasks = a.N * g.strips;
+    g.we = 2 * g.pq + 4;
     g.wb = 2 * g.pq + 1; g.hb = 2; g.nb = 1;
-    g.we = g.wb + 3;                          // 4x4 taps over the padded s2d map
-    if (2 * g.we > BM) return cudaErrorInvalidValue;
     g.tiles_w = 1; g.tiles_h = 1;
     g.m_tiles = g.n_tasks * g.ph;
     g.cblocks = 1;
-    g.k_chunks = a.KH * a.KW;                 // 4 x 64 = 256 = 16 taps x 16 (resident B size)
-    g.a_bytes = 2 * (16 * g.we * 5);          // two planes of 5 rows x we pixels x 16 B
+    g.k_chunks = 5;                            // resident weights: 5 x 16 KB = 20 chunks x 4 KB
+    g.a_bytes = 2 * (16 * g.we * 2 * M8_ROWS); // two planes of [5 rows][2 strips][we] x 16 B
     {
-      const int plane_stride = (g.a_bytes / 2 + 127) / 128 * 128;
-      const int rows_read = BM + 3 * g.we + 3;  // by the last tap (rows past the box: garbage rows)
-      g.a_stage_bytes = (plane_stride + rows_read * 16 + 1023) / 1024 * 1024;
+      // the MMA of the last row reads 128 rows + 3 shifted columns past that row's start
+      const int plane = ((M8_ROWS - 1) * 2 * g.we + 128 + 3) * 16;
+      const int pstride = (plane + 127) / 128 * 128;
+      g.a_stage_bytes = 2 * pstride;
     }
-    g.a_stages = MAX_A_STAGES;
-    g.ring_bytes = (M8_RING * g.wb * 128 + 1023) / 1024 * 1024;
+    g.a_stages = 4;
+    g.ring_bytes = 2 * 2 * g.we * 128;         // two buffers of vertically pooled rows
     g.tma_out = 0;
   } else if (mode == 6) {
     // halo tile: full output rows (wb = OW), hb rows, one image; extended width we = OW + KW - 1

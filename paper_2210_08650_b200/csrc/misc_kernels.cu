@@ -62,19 +62,22 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 }
 
 // ---------------------------------------------------------------- pack_input
-__global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout) {
+__global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout,
+                                  int wp) {
   griddep_launch_dependents();
   griddep_wait();
   const int HW = H * W;
   if (layout == 2) {
-    // space-to-depth 2x2 with a zero border (2 before, 1 after) so the stem's 4x4 window
-    // view never leaves the buffer: one thread per padded pixel of the (H/2+3) x (W/2+3) grid
-    const int H2 = H / 2, W2 = W / 2, HP = H2 + 3, WP = W2 + 3;
+    // space-to-depth 2x2 with a zero border (rows: 2 before, 1 after; columns: 3 before, 1
+    // after) so the stem's 4x4 windows -- and the stem+pool kernel's boxes, which start one
+    // column left of the stem's first column -- never leave the buffer: one thread per padded
+    // pixel of the (H/2+3) x (W/2+4) grid
+    const int H2 = H / 2, W2 = W / 2, HP = H2 + 3, WP = wp;
     const long long total = (long long)N * HP * WP;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
       const long long n = t / (HP * WP);
       const int rem = (int)(t - n * HP * WP);
-      const int i = rem / WP - 2, j = rem - (rem / WP) * WP - 2;
+      const int i = rem / WP - 2, j = rem - (rem / WP) * WP - 3;
       float v[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) v[c] = 0.f;
@@ -313,9 +316,9 @@ cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int
   return cudaGetLastError();
 }
 
-cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, cudaStream_t st) {
-  const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * (W / 2 + 3) : (long long)N * H * W;
-  launch_pdl(pack_input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, img, y, N, H, W, layout);
+cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, int wp, cudaStream_t st) {
+  const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * wp : (long long)N * H * W;
+  launch_pdl(pack_input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, img, y, N, H, W, layout, wp);
   return cudaGetLastError();
 }
 

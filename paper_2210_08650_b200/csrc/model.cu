@@ -141,7 +141,7 @@ struct ConvW {
   int cout = 0, kh = 1, kw = 1, stride = 1, pad = 0;
   int K = 0, Kp = 0;
   void* w = nullptr;           // bf16 [Cout][Kp] (tc) or fp32 [K][Cout] (simt)
-  void* w8 = nullptr;          // s2d stem, mode 8: bf16 [tap 16][k half 2][n 64][8] (no-swizzle K-major)
+  void* w8 = nullptr;          // s2d stem, mode 8: bf16 [chunk 20][k half 2][n 128][8] (no-swizzle K-major)
   float* bias = nullptr;       // [Cout]
   float* pro_scale = nullptr;  // [cs]
   float* pro_shift = nullptr;
@@ -422,13 +422,20 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     if (st != HAPI_OK) return st;
     cw.w = dw;
     if (s.s2d && s.cout <= 64) {
-      // one 16-channel tap per MMA (K = 16): [tap][k half][n][8] = core matrices of 8 n x 16 B
-      std::vector<uint16_t> h8((size_t)taps * 2 * 64 * 8, 0);
-      for (int tap = 0; tap < taps; ++tap)
-        for (int kh = 0; kh < 2; ++kh)
-          for (int o = 0; o < s.cout; ++o)
-            for (int j = 0; j < 8; ++j)
-              h8[(((size_t)tap * 2 + kh) * 64 + o) * 8 + j] = hw[(size_t)o * cw.Kp + tap * 16 + kh * 8 + j];
+      // stem+pool kernel (mode 8): 20 K chunks (padded s2d row rho 0..4, tap column s 0..3) of
+      // [k half 2][n 128][8] (no-swizzle core matrices): n < 64 computes stem row 2po with tap
+      // row rho, n >= 64 stem row 2po+1 with tap row rho-1; zero where the tap row is outside 0..3
+      std::vector<uint16_t> h8((size_t)20 * 2 * 128 * 8, 0);
+      for (int rho = 0; rho < 5; ++rho)
+        for (int sc = 0; sc < 4; ++sc)
+          for (int kh = 0; kh < 2; ++kh)
+            for (int n = 0; n < 128; ++n) {
+              const int o = n & 63, r = n < 64 ? rho : rho - 1;
+              if (o >= s.cout || r < 0 || r > 3) continue;
+              for (int j = 0; j < 8; ++j)
+                h8[((((size_t)(rho * 4 + sc)) * 2 + kh) * 128 + n) * 8 + j] =
+                    hw[(size_t)o * cw.Kp + (r * 4 + sc) * 16 + kh * 8 + j];
+            }
       uint16_t* d8;
       if ((st = upload(m, h8, &d8)) != HAPI_OK) return st;
       cw.w8 = d8;
@@ -643,7 +650,11 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   const int layout = !m->bf16 ? 0 : (s2d ? 2 : 1);
   View cur;
   if (start == 0) {
-    cur = layout == 2 ? b.compact(16, H0 / 2 + 3, W0 / 2 + 3) : b.compact(layout == 1 ? 8 : 3, H0, W0);
+    // s2d padded width: 3 zero columns on the left, >= 1 on the right, and room for the
+    // stem+pool kernel's last strip box (S strips of 2 pq stem columns, box width 2 pq + 4)
+    const int sw = W0 / 2, spw = (sw - 1) / 2 + 1, sS = (spw + 29) / 30, spq = (spw + sS - 1) / sS;
+    const int WP = std::max(sw, 2 * sS * spq) + 4;
+    cur = layout == 2 ? b.compact(16, H0 / 2 + 3, WP) : b.compact(layout == 1 ? 8 : 3, H0, W0);
     Op o;
     o.t = OP_PACK_IN;
     o.out = cur;
@@ -699,7 +710,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           if (!m->convs[op->conv].w8) return set_error(HAPI_ERR_UNSUPPORTED, "stem weights for mode 8 missing");
           op->tc_mode = 8;
           op->conv_oh = oh; op->conv_ow = ow;
-          const int pw = o.W, strips = (pw + 30) / 31, pq = (pw + strips - 1) / strips;
+          const int pw = o.W, strips = (pw + 29) / 30, pq = (pw + strips - 1) / strips;
           op->wb = 2 * pq + 1; op->hb = 2; op->nb = 1;
           const ConvW& w = m->convs[op->conv];
           op->flops = w.real_flops_per_px * (double)oh * ow;
@@ -1074,7 +1085,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
   const int isb = m->bf16 ? 1 : 0;
   switch (o.t) {
     case OP_PACK_IN:
-      e = pack_input_launch(images, vptr(m, p, o.out, out), nb, (int)m->d.in_h, (int)m->d.in_w, o.layout, st);
+      e = pack_input_launch(images, vptr(m, p, o.out, out), nb, (int)m->d.in_h, (int)m->d.in_w, o.layout, o.out.W, st);
       break;
     case OP_UNPACK:
       e = unpack_nchw_launch(images, nb, o.out.C, o.out.H * o.out.W, vptr(m, p, o.out, out), o.out.ld, m->es, st);
@@ -1141,7 +1152,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
         mp.bh = w.has_half ? &w.tmap_half : nullptr;
         mp.y = o.nchw_out ? nullptr : &o.tmap_y;
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
-        e = conv_tc_launch(a, mp, w.bn, o.tc_mode, o.wb, o.hb, o.nb, m->num_sms, st);
+        e = conv_tc_launch(a, mp, o.tc_mode == 8 ? 128 : w.bn, o.tc_mode, o.wb, o.hb, o.nb, m->num_sms, st);
       } else {
         a.ksplit = o.ksplit;
         a.ws = o.ksplit > 1 ? reinterpret_cast<float*>(vptr(m, p, o.ws, out)) : nullptr;
@@ -1282,20 +1293,24 @@ hapi_status finalize_tmaps(hapi_model* m) {
         if ((st = encode_view(m, p, o, o.out2, 64, &o.tmap_y2, "Y2")) != HAPI_OK) return st;
       }
       if (o.tc_mode == 8) {
-        // halo box over the padded s2d input [N][HP][WP][16]: {8 channels, wb + 3, 2 + 3, 1},
-        // loaded twice (channels 0-7, 8-15) into two 16-byte-per-pixel planes
+        // stem+pool boxes over the padded s2d input [N][HP][WP][16] as a 5D view
+        // {16 ch, we cols, S strips (stride 2 pq cols), HP rows, N}: one box {8, we, 2, 5, 1}
+        // per 8-channel plane lands as [row][strip][col] x 16 B.  Column x of strip k is
+        // padded column 2 k pq + x = stem column 2 k pq - 1 + x (3 zero columns on the left).
+        const int pw = o.out.W, S = (pw + 29) / 30, pq = (pw + S - 1) / S, we = 2 * pq + 4;
         void* base = vptr(m, p, o.in, nullptr);
         const cuuint64_t px = (cuuint64_t)o.in.ld * 2;
-        cuuint64_t dims[4] = {16, (cuuint64_t)o.in.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
-        cuuint64_t strides[3] = {px, px * o.in.W, px * o.in.W * o.in.H};
-        cuuint32_t box[4] = {8, (cuuint32_t)(o.wb + 3), 5, 1};
-        cuuint32_t estr[4] = {1, 1, 1, 1};
-        st = encode_bf16(&o.tmap_a, 4, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_NONE, o.desc + " stem halo");
+        cuuint64_t dims[5] = {16, (cuuint64_t)we, (cuuint64_t)S, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+        cuuint64_t strides[4] = {px, px * 2 * pq, px * o.in.W, px * o.in.W * o.in.H};
+        cuuint32_t box[5] = {8, (cuuint32_t)we, 2, 5, 1};
+        cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+        st = encode_bf16(&o.tmap_a, 5, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_NONE, o.desc + " stem 5D");
         if (st != HAPI_OK) return st;
       } else if (o.s2d_view) {
         // overlapping window view of the padded s2d input: element (e, w, h, n) at
-        // base + n*HP*WP*32 + h*WP*32 + w*32 + 2e, e < 64 spans 4 adjacent pixels
-        void* base = vptr(m, p, o.in, nullptr);
+        // base + n*HP*WP*32 + h*WP*32 + (w+1)*32 + 2e, e < 64 spans 4 adjacent pixels (stem
+        // column w starts at padded column w+1: the buffer has 3 zero columns on the left)
+        void* base = static_cast<char*>(vptr(m, p, o.in, nullptr)) + o.in.ld * 2;
         const cuuint64_t px = (cuuint64_t)o.in.ld * 2;  // 32 B
         const int stem_w = o.tc_mode == 8 ? o.conv_ow : o.out.W;
         cuuint64_t dims[4] = {64, (cuuint64_t)stem_w, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
