@@ -338,31 +338,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // swizzled 16-byte smem reads, one 16-byte global store.
     const int pt = threadIdx.x - M8_POOL_WARP0 * 32;
     __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.y);
-    const int items = 2 * g.pq * 8;
+    // this thread's items (strip k, pooled column qo, channel group cg) are the same in every
+    // tile: their smem offsets and pooled-column offsets are computed once
+    constexpr int M8_MAX_ITEMS = 6;            // ceil(2 x 30 x 8 / 96)
+    uint32_t off[M8_MAX_ITEMS][3];
+    int qcol[M8_MAX_ITEMS], cgo[M8_MAX_ITEMS];
+    int n_items = 0;
+    for (int item = pt; item < 2 * g.pq * 8 && n_items < M8_MAX_ITEMS; item += M8_POOL_THREADS, ++n_items) {
+      const int k = item / (g.pq * 8), rem = item - k * (g.pq * 8);
+      const int qo = rem >> 3, cg = rem & 7;
+#pragma unroll
+      for (int dc = 0; dc < 3; ++dc) {
+        const int x = 2 * qo + dc;
+        off[n_items][dc] = (uint32_t)((k * g.we + x) * 128 + ((cg ^ (x & 7)) << 4));
+      }
+      qcol[n_items] = k * g.pq + qo;
+      cgo[n_items] = cg * 8;
+    }
     int po = 0, task = blockIdx.x;
     for (int it = 0; task < g.n_tasks; ++it) {
       const int img = task / g.strips, pair = task - img * g.strips;
       mbar_wait(&pready[it & 1], (it >> 1) & 1);
       const uint32_t vbuf = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2));
-      for (int item = pt; item < items; item += M8_POOL_THREADS) {
-        const int k = item / (g.pq * 8), rem = item - k * (g.pq * 8);
-        const int qo = rem >> 3, cg = rem & 7;
-        const int q = (2 * pair + k) * g.pq + qo;
-        if (qo >= g.pq || q >= g.pw) continue;
+      __nv_bfloat16* yrow = yb + (((long long)img * g.ph + po) * g.pw + 2 * pair * g.pq) * a.y_ld;
+      const int qlim = g.pw - 2 * pair * g.pq;
+#pragma unroll
+      for (int i = 0; i < M8_MAX_ITEMS; ++i) {
+        if (i >= n_items || qcol[i] >= qlim) continue;
         uint32_t mx[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int dc = 0; dc < 3; ++dc) {
-          const int x = 2 * qo + dc;
-          const uint32_t addr = vbuf + (uint32_t)((k * g.we + x) * 128 + ((cg ^ (x & 7)) << 4));
           uint32_t u[4];
           asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
                        : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
-                       : "r"(addr));
+                       : "r"(vbuf + off[i][dc]));
 #pragma unroll
           for (int j = 0; j < 4; ++j) mx[j] = bf16x2_max(mx[j], u[j]);
         }
-        *reinterpret_cast<uint4*>(yb + (((long long)img * g.ph + po) * g.pw + q) * a.y_ld + cg * 8) =
-            make_uint4(mx[0], mx[1], mx[2], mx[3]);
+        *reinterpret_cast<uint4*>(yrow + (long long)qcol[i] * a.y_ld + cgo[i]) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
       }
       mbar_arrive(&pfree[it & 1]);
       if (++po == g.ph) {
@@ -390,12 +403,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       prev[j] = 0.f;
     }
     int po = 0, task = blockIdx.x;
+    float bv0[32], bv1[32];  // bias, or -inf where the stem position is padding (max ignores it)
     for (int it = 0; task < g.n_tasks; ++it) {
       const int acc = it & 1;
       const int pair = task % g.strips;
       const int stem_col = 2 * (2 * pair + k) * g.pq - 1 + x;
       const bool valid = live && stem_col >= 0 && stem_col < a.OW;
       const bool valid1 = valid && 2 * po + 1 < a.OH;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        bv0[j] = valid ? bias[j] : -INFINITY;
+        bv1[j] = valid1 ? bias[j] : -INFINITY;
+      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       uint32_t v0[32], v1[32];
@@ -416,11 +435,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float f[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+              // prev >= 0, so max(prev, a, b) = max(prev, relu(a), relu(b)); padding is -inf
               const int c = c4 * 8 + 2 * j + h;
-              const float r0 = valid ? fmaxf(__uint_as_float(v0[c]) + bias[c], 0.f) : 0.f;
-              const float r1 = valid1 ? fmaxf(__uint_as_float(v1[c]) + bias[c], 0.f) : 0.f;
-              f[h] = fmaxf(fmaxf(prev[c], r0), r1);
-              prev[c] = r1;
+              const float a0 = __uint_as_float(v0[c]) + bv0[c];
+              const float a1 = __uint_as_float(v1[c]) + bv1[c];
+              f[h] = fmaxf(fmaxf(prev[c], a0), a1);
+              prev[c] = fmaxf(a1, 0.f);
             }
             o[j] = pack_bf16x2(f[0], f[1]);
           }
