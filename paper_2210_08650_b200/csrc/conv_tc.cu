@@ -50,8 +50,8 @@ constexpr int MMA_WARP = 12;
 constexpr int RES_WARP = 13;
 constexpr int XFORM_TMA_WARP = 14;   // mode 7: TMA issuer while warps 8-11 transform
 constexpr int NUM_THREADS = 15 * 32;
-constexpr int M8_POOL_WARP0 = 9;      // mode 8: warps 9-11 pool while 0-7 drain TMEM
-constexpr int M8_POOL_THREADS = 96;
+constexpr int M8_POOL_WARP0 = 9;      // mode 8: warps 9-11, 13, 14 pool while 0-7 drain TMEM
+constexpr int M8_POOL_THREADS = 160;
 constexpr int M8_ROWS = 5;            // mode 8: padded s2d rows per tile (2 stem rows + 3 taps)
 constexpr int M8_CHUNKS = M8_ROWS * 4; // mode 8: K chunks (s2d row x tap column), K = 16 each
 constexpr int A_STAGE_BYTES = BM * BK * 2;
@@ -330,17 +330,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (MODE == 8 && warp >= M8_POOL_WARP0 && warp < PROD_WARP0 + 4) {
+  } else if (MODE == 8 && ((warp >= M8_POOL_WARP0 && warp < PROD_WARP0 + 4) || warp == RES_WARP ||
+                            warp == XFORM_TMA_WARP)) {
     // ================================================================ mode 8 pooling
     // Horizontal half of the 3x3/s2/p1 max: the epilogue already took the vertical max over
     // stem rows 2po-1..2po+1 into V (one row per strip column); pooled column q of strip k =
     // max(V[2qo], V[2qo+1], V[2qo+2]).  Item = (strip, pooled column, 8-channel group): three
     // swizzled 16-byte smem reads, one 16-byte global store.
-    const int pt = threadIdx.x - M8_POOL_WARP0 * 32;
+    const int pt = (warp < PROD_WARP0 + 4 ? warp - M8_POOL_WARP0 : warp - RES_WARP + 3) * 32 + lane;
     __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.y);
     // this thread's items (strip k, pooled column qo, channel group cg) are the same in every
     // tile: their smem offsets and pooled-column offsets are computed once
-    constexpr int M8_MAX_ITEMS = 6;            // ceil(2 x 30 x 8 / 96)
+    constexpr int M8_MAX_ITEMS = 3;            // ceil(2 x 30 x 8 / 160)
     uint32_t off[M8_MAX_ITEMS][3];
     int qcol[M8_MAX_ITEMS], cgo[M8_MAX_ITEMS];
     int n_items = 0;
