@@ -737,13 +737,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&afull[ast], aph);
           tc_fence_after();
           if (elect_one()) {
-            const uint32_t a_base = sA0 + ast * ASZ;
-#pragma unroll 1
-            for (int t = 0; t < M8_CHUNKS; ++t) {
-              const int rho = t >> 2, sft = t & 3;
-              const uint64_t adesc = make_sdesc_none(a_base + rho * row_stride + (uint32_t)sft * 16u, plane_stride, 128);
-              const uint64_t bdesc = make_sdesc_none(sB0 + t * 4096, 2048, 128);
-              mma_bf16(d_tmem, adesc, bdesc, idesc, t != 0);
+            // descriptors built once and advanced by adds (start-address field, 16-byte units):
+            // a single lane issues the 20 MMAs back to back
+            const uint64_t a0 = make_sdesc_none(sA0 + ast * ASZ, plane_stride, 128);
+            const uint64_t b0 = make_sdesc_none(sB0, 2048, 128);
+            const uint32_t rs16 = row_stride >> 4;
+#pragma unroll
+            for (int rho = 0; rho < M8_ROWS; ++rho) {
+#pragma unroll
+              for (int sft = 0; sft < 4; ++sft)
+                mma_bf16(d_tmem, a0 + rho * rs16 + sft, b0 + (rho * 4 + sft) * 256, idesc, (rho | sft) != 0);
             }
             mma_commit(&aempty[ast]);
             mma_commit(&tfull[acc]);
