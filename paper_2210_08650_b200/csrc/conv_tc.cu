@@ -181,14 +181,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
   // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
+  // MODE 10 = im2col mode 5 with two M sub-tiles per weight stage
   constexpr bool HALO = (MODE == 6 || MODE == 9);
-  constexpr int MT = MODE == 9 ? 2 : 1;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || MODE == 5 || HALO || MODE == 7 || MODE == 8);
+  constexpr bool IM2COL = (MODE == 5 || MODE == 10);
+  constexpr int MT = (MODE == 9 || MODE == 10) ? 2 : 1;
+  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   const int S = g.stages;
   const int AS = (HALO || MODE == 8) ? g.a_stages : S;
   constexpr int CPS = (MODE == 3 && BN <= 128) ? 2 : 1;  // == g.cps (host); mode 4 measured better at 1
-  const int ASZ = HALO ? MT * g.a_stage_bytes : MODE == 8 ? g.a_stage_bytes : CPS * A_STAGE_BYTES;  // A slot
+  const int ASZ = HALO ? MT * g.a_stage_bytes : MODE == 8 ? g.a_stage_bytes : MT * CPS * A_STAGE_BYTES;  // A slot
   const int BSZ = CPS * C::B_STAGE_BYTES;                               // B ring slot
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -540,13 +542,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (warp == PROD_WARP0) {
         uint32_t stage = 0, phase = 0;
         for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
-          const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+          const int tm = (tile / g.n_tiles) * MT, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+          // (MT == 1: always one, even for the out-of-range partner tile of an odd multicast pair)
+          const int nsub = MT == 1 ? 1 : (g.m_tiles - tm < MT ? g.m_tiles - tm : MT);
           int ow0 = 0, oh0 = 0, b0 = 0, w0 = 0, h0 = 0;
+          int w1 = 0, h1 = 0, b1 = 0;  // MODE 10: origin of the second M sub-tile
           if (SPATIAL) {
             tile_origin(g, tm, &ow0, &oh0, &b0);
             w0 = ow0 * a.stride - a.pad;
             h0 = oh0 * a.stride - a.pad;
-          } else if (MODE == 5) {
+          } else if (IM2COL) {
             // flat tile: its first output pixel (n, oh, ow) -> im2col start position
             const long long m0 = (long long)tm * BM;
             b0 = (int)(m0 / OHW);
@@ -555,13 +560,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ow0 = rem - oh0 * a.OW;
             w0 = ow0 * a.stride - a.pad;
             h0 = oh0 * a.stride - a.pad;
+            if (MT > 1) {
+              const long long m1 = m0 + BM;
+              b1 = (int)(m1 / OHW);
+              const int rem1 = (int)(m1 - (long long)b1 * OHW);
+              const int oh1 = rem1 / a.OW, ow1 = rem1 - (rem1 / a.OW) * a.OW;
+              w1 = ow1 * a.stride - a.pad;
+              h1 = oh1 * a.stride - a.pad;
+            }
           }
           int cb = 0, r = 0, sft = 0;  // (tap, channel block) of chunk kc, tracked incrementally
           for (int kc = 0; kc < g.k_chunks; kc += CPS) {
             const int nch = g.k_chunks - kc < CPS ? g.k_chunks - kc : CPS;
             mbar_wait(&empty[stage], phase ^ 1);
             if (elect_one()) {
-              mbar_arrive_expect_tx(&full[stage], nch * (g.a_bytes + (g.b_res ? 0 : C::B_STAGE_BYTES)));
+              mbar_arrive_expect_tx(&full[stage], nch * (nsub * g.a_bytes + (g.b_res ? 0 : C::B_STAGE_BYTES)));
               int cb_j = cb, r_j = r, s_j = sft;
               for (int j = 0; j < nch; ++j) {
                 const int ck = kc + j;
@@ -573,14 +586,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   const int c2 = ck - g.k1_chunks + (a.k2_diag ? tn * (BN / BK) : 0);
                   if (MODE == 3)
                     tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
-                  else if (MODE == 5)
+                  else if (IM2COL)
                     tma_load_im2col_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, 0, 0, &full[stage]);
                   else
                     tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
                 } else if (MODE == 3) {
                   tma_load_2d(dA, &tmap_a, ck * BK, tm * BM, &full[stage]);
-                } else if (MODE == 5) {
+                } else if (IM2COL) {
                   tma_load_im2col_4d(dA, &tmap_a, cb_j * BK, w0, h0, b0, (uint16_t)s_j, (uint16_t)r_j, &full[stage]);
+                  if (MT > 1 && nsub > 1)
+                    tma_load_im2col_4d(dA + A_STAGE_BYTES, &tmap_a, cb_j * BK, w1, h1, b1, (uint16_t)s_j, (uint16_t)r_j,
+                                       &full[stage]);
                 } else {
                   tma_load_4d(dA, &tmap_a, cb_j * BK, w0 + s_j, h0 + r_j, b0, &full[stage]);
                 }
@@ -725,7 +741,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const uint32_t acc_phase = (iter >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * MT * BN;
+        const int nsub_mma = MT > 1 ? (g.m_tiles - (tile / g.n_tiles) * MT < MT ? g.m_tiles - (tile / g.n_tiles) * MT : MT) : 1;
         if (MODE == 8) {
           // 20 K chunks (s2d row rho, tap column s), K = 16 each, N = 128 = both stem rows of
           // the tile (row 2po uses tap row rho, row 2po+1 tap row rho-1; the weight block holds
@@ -848,6 +865,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int k = 0; k < BK / 16; ++k) {
                 // advance 16 bf16 = 32 bytes along K inside the 128-byte swizzle atom
                 mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kc + j) | k) != 0);
+              }
+              if (MT > 1 && nsub_mma > 1) {  // MODE 10: the second M sub-tile shares the weight chunk
+                const uint64_t adesc1 = adesc + (A_STAGE_BYTES >> 4);
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k)
+                  mma_bf16(d_tmem + BN, adesc1 + 2 * k, bdesc + 2 * k, idesc, ((kc + j) | k) != 0);
               }
             }
             if (g.mc)
@@ -1129,20 +1152,21 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
       smem = a_ring + g.stages * C::B_STAGE_BYTES + C::FIXED + res_bytes;
     }
   } else if (g.b_res) {
-    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - bres_bytes) / (g.cps * A_STAGE_BYTES);
+    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - bres_bytes) / (g.cps * g.mt * A_STAGE_BYTES);
     if (g.stages > MAX_STAGES) g.stages = MAX_STAGES;
-    smem = g.stages * g.cps * A_STAGE_BYTES + bres_bytes + C::FIXED + res_bytes;
+    smem = g.stages * g.cps * g.mt * A_STAGE_BYTES + bres_bytes + C::FIXED + res_bytes;
   } else {
-    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - pro_bytes) / (g.cps * C::STAGE_BYTES);
+    const int stage_bytes = g.cps * (g.mt * A_STAGE_BYTES + C::B_STAGE_BYTES);
+    g.stages = (SMEM_LIMIT - C::FIXED - res_bytes - pro_bytes) / stage_bytes;
     if (g.stages > MAX_STAGES) g.stages = MAX_STAGES;
-    smem = g.stages * g.cps * C::STAGE_BYTES + C::FIXED + res_bytes + pro_bytes;
+    smem = g.stages * stage_bytes + C::FIXED + res_bytes + pro_bytes;
   }
   if (g.stages < 2 && !(g.mode == 6 && g.b_res)) return cudaErrorInvalidValue;
   // 2-CTA clusters with multicast weights: the generic TMA path, weights streamed (not
   // resident), no identity block, at least two M tiles; every weight chunk then crosses L2
   // once per CTA pair instead of once per CTA
   g.mc = 0;
-  if ((g.mode == 3 || g.mode == 4 || g.mode == 5) && !g.b_res && !a.k2_diag && BN >= 128 && mp.bh &&
+  if ((g.mode == 3 || g.mode == 4 || g.mode == 5) && g.mt == 1 && !g.b_res && !a.k2_diag && BN >= 128 && mp.bh &&
       g.m_tiles >= 2 && cluster_enabled()) {
     g.mc = 1;
     g.n_pairs = (g.m_tiles + 1) / 2 * g.n_tiles;
@@ -1181,7 +1205,12 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 2: return launch_t<BN, 2>(a, g, mp, num_sms, st);
     case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
-    case 5: return launch_t<BN, 5>(a, g, mp, num_sms, st);
+    case 5:
+      if (g.mt == 2) {
+        if constexpr (BN <= 128) return launch_t<BN, 10>(a, g, mp, num_sms, st);
+        return cudaErrorInvalidValue;
+      }
+      return launch_t<BN, 5>(a, g, mp, num_sms, st);
     case 6:
       if (g.mt == 2) {
         if constexpr (BN <= 128) return launch_t<BN, 9>(a, g, mp, num_sms, st);
@@ -1309,6 +1338,9 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
       g.pro_c = (a.C + BK - 1) / BK * BK;
     }
   }
+  // im2col convs at BN = 128: two M sub-tiles share every weight chunk (halves the L2 weight
+  // stream; TMEM 2 x 2 x 128 columns)
+  if (mode == 5 && bn == 128 && g.n_tiles == 1 && !a.res && a.k2_chunks == 0 && dual_m_enabled()) g.mt = 2;
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {
     if ((mode != 3 && mode != 4 && mode != 5) || !mp.a2 || (a.k2_diag && (!mp.b2 || bn > 256))) return cudaErrorInvalidValue;
