@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(P_THREADS, 1)
         } else if (a.k2_diag) {
           const int c = kc - a.k1_chunks;  // residual channels j*128 + 64c against identity chunk c
           tma_load_2d(dA, &tm_a2, j * BN1 + c * PK, row0, bar);
-          tma_load_2d(dB, &tm_id, c * PK, 0, bar);
+          tma_load_2d(dB, &tm_id, 0, -c * PK, bar);
         } else {
           const int c = kc - a.k1_chunks;  // fused 1x1 downsample: its weights follow W3's K columns
           tma_load_2d(dA, &tm_a2, c * PK, row0, bar);
@@ -247,8 +247,22 @@ __global__ void __launch_bounds__(P_THREADS, 1)
     const uint32_t stg0 = smem_u32(stg);
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     int n = 0, it = 0;
+    const int sub_w = (a.W + 1) >> 1, sub_h = (a.H + 1) >> 1;
     for (int tile = blockIdx.x; tile < m_tiles; tile += gridDim.x, ++it) {
       const int row0 = tile * PM;
+      // y1_sub: this thread's pixel, if it is an even (row, col) one, goes to the compact map
+      uint8_t* dsub = nullptr;
+      if (a.y1_sub) {
+        const long long m = (long long)row0 + row;
+        if (m < a.M) {
+          const long long hw = (long long)a.H * a.W;
+          const long long nimg = m / hw;
+          const int rem = (int)(m - nimg * hw), oh = rem / a.W, ow = rem - (rem / a.W) * a.W;
+          if (!((oh | ow) & 1))
+            dsub = static_cast<uint8_t*>(a.y1_sub) +
+                   (((nimg * sub_h + (oh >> 1)) * sub_w + (ow >> 1)) * a.cout1 + gsel * 32) * 2;
+        }
+      }
       for (int j = 0; j < nt1; ++j, ++n) {
         const int buf = n & 1;
         mbar_wait(&tfull1[buf], (n >> 1) & 1);
@@ -279,6 +293,8 @@ __global__ void __launch_bounds__(P_THREADS, 1)
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(blk + swz_off<128>(row, gsel * 4 + c4)),
                          "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
                          : "memory");
+            if (dsub)
+              *reinterpret_cast<uint4*>(dsub + (j * BN1 + b * 64 + c4 * 8) * 2) = make_uint4(o[0], o[1], o[2], o[3]);
           }
         }
         tc_fence_before();
@@ -287,8 +303,9 @@ __global__ void __launch_bounds__(P_THREADS, 1)
         mbar_arrive(&a2full[buf]);
         epi_bar();
         if (et == 0) {
-          for (int b = 0; b < 2; ++b)
-            tma_store_2d(&tm_y1, stg0 + (buf * 2 + b) * P_STG_BYTES, j * BN1 + b * 64, row0);
+          if (!a.y1_sub)
+            for (int b = 0; b < 2; ++b)
+              tma_store_2d(&tm_y1, stg0 + (buf * 2 + b) * P_STG_BYTES, j * BN1 + b * 64, row0);
           bulk_commit();
         }
       }

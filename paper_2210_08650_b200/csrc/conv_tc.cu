@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         mbar_arrive_expect_tx(bres, (uint32_t)g.k_chunks * C::B_STAGE_BYTES);
         for (int c = 0; c < g.k_chunks; ++c) {
           if (a.k2_diag && c >= g.k1_chunks)
-            tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b2, (c - g.k1_chunks) * BK, 0, bres);
+            tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b2, 0, -(c - g.k1_chunks) * BK, bres);
           else
             tma_load_2d(smem_u32(sB + c * C::B_STAGE_BYTES), &tmap_b, c * BK, 0, bres);
         }
@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (!g.b_res) {
                   const uint32_t dB = smem_u32(sB + stage * BSZ + j * C::B_STAGE_BYTES);
                   if (a.k2_diag && ck >= g.k1_chunks)
-                    tma_load_2d(dB, &tmap_b2, (ck - g.k1_chunks) * BK, 0, &full[stage]);
+                    tma_load_2d(dB, &tmap_b2, 0, -(ck - g.k1_chunks) * BK, &full[stage]);
                   else if (g.mc)  // my half of the weight chunk, multicast into both CTAs
                     tma_load_2d_mc(dB + (blockIdx.x & 1) * (BN / 2) * 128, &tmap_bh, ck * BK,
                                    tn * BN + (int)(blockIdx.x & 1) * (BN / 2), &full[stage], 3);

@@ -92,7 +92,7 @@ struct ConvArgs {
 struct ConvMaps {
   const CUtensorMap* a;  // A operand (modes 3/4) or nullptr
   const CUtensorMap* a2; // second A source (k2_chunks > 0) or nullptr
-  const CUtensorMap* b2; // k2_diag: the shared 256x256 bf16 identity, box {64, BN}
+  const CUtensorMap* b2; // k2_diag: the shared 64x64 bf16 identity block, box {64, BN}, loaded at row -64c
   const CUtensorMap* b;  // weights
   const CUtensorMap* bh; // weights with a {64, bn/2} box (2-CTA multicast halves) or nullptr
   const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
@@ -108,12 +108,15 @@ struct PairArgs {
   int cout1;            // conv3 output channels (multiple of 128, <= 2048)
   const float* bias1;   // [cout1] conv3 bias (+ ds bias)
   const float* bias2;   // [n2] next conv1 bias
+  void* y1_sub;         // non-null: store the block output only at even (row, col) pixels, as a
+                        // compact [N][(H+1)/2][(W+1)/2][cout1] bf16 tensor (y1 map unused)
+  int H, W;             // pixel grid of the M rows (for y1_sub)
 };
 struct PairMaps {
   const CUtensorMap* a1;  // t2 [M][K1], box {64, 128}
   const CUtensorMap* a2;  // residual / ds input [M][C2], box {64, 128}
   const CUtensorMap* b1;  // conv3 weights [cout1][Kp], box {64, 128}
-  const CUtensorMap* id;  // 256x256 identity, box {64, 128}
+  const CUtensorMap* id;  // 64x64 identity block, box {64, 128}, loaded at row -64c
   const CUtensorMap* b2;  // next conv1 weights [n2][cout1], box {64, n2}
   const CUtensorMap* y1;  // block output view [M][cout1], box {64, 128}, 128B swizzle
   const CUtensorMap* y2;  // next conv1 output view [M][n2], box {64, 128}, 128B swizzle

@@ -111,6 +111,14 @@ bool pair_enabled() {
   return on;
 }
 
+bool sub_store_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_SUB_STORE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool res_identity_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_RES_GEMM");
@@ -191,6 +199,12 @@ struct Op {
   CUtensorMap tmap_y2;
   int ksplit = 1;                // fp32 SIMT split-K slices (partial sums in `ws`)
   View ws;
+  // OP_PAIR whose block output is read only by a later 1x1/stride-2 downsample: `out` holds
+  // just the even (row, col) pixels of the full_h x full_w map, the consumer reads it with
+  // in2_stride = 1
+  bool sub_out = false;
+  int full_h = 0, full_w = 0;
+  int in2_stride = 0;            // 0: the conv's own stride2
 };
 
 struct Buf {
@@ -224,7 +238,7 @@ struct hapi_model {
   int64_t weight_bytes = 0;
   uint32_t start = 0;                          // suffix models: input = layer `start` output
   int64_t in_bytes_per_img = 0;                // suffix models: bytes of one input activation
-  void* ident = nullptr;                       // shared 256x256 bf16 identity (residual in GEMM)
+  void* ident = nullptr;                       // shared 64x64 bf16 identity block (residual in GEMM)
   CUtensorMap ident_map128, ident_map256;      // box {64, 128} / {64, 256}
   std::vector<Plan> plans;  // index split - min_split
   void* arena = nullptr;
@@ -444,15 +458,17 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     if (s.res_identity) {
       if (cw.bn != 128 && cw.bn != 256) return set_error(HAPI_ERR_UNSUPPORTED, "identity residual needs BN 128/256");
       if (!m->ident) {
-        std::vector<uint16_t> id(256 * 256, 0);
-        for (int i = 0; i < 256; ++i) id[(size_t)i * 256 + i] = 0x3F80;  // bf16 1.0
+        // one 64x64 block: K chunk c of the N-row identity is this block at row offset c*64,
+        // loaded at row coordinate -c*64 (the rows outside it are TMA out-of-bounds zeros)
+        std::vector<uint16_t> id(64 * 64, 0);
+        for (int i = 0; i < 64; ++i) id[(size_t)i * 64 + i] = 0x3F80;  // bf16 1.0
         uint16_t* did;
         if ((st = upload(m, id, &did)) != HAPI_OK) return st;
         m->ident = did;
         EncodeTiledFn enc0 = get_encode_fn();
         if (!enc0) return set_error(HAPI_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        cuuint64_t dims[2] = {256, 256};
-        cuuint64_t strides[1] = {512};
+        cuuint64_t dims[2] = {64, 64};
+        cuuint64_t strides[1] = {128};
         cuuint32_t estr[2] = {1, 1};
         for (int bn2 : {128, 256}) {
           cuuint32_t box[2] = {64, (cuuint32_t)bn2};
@@ -1022,6 +1038,40 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     op.bytes = 2.0 * cur.C * cur.H * cur.W * m->es;
     b.emit(op);
   }
+  // A pair's block output whose only other reader is the next stage's fused 1x1/stride-2
+  // downsample is stored at stride 2 (a quarter of the bytes; the pair's GEMM2 takes the full
+  // tile from shared memory either way).
+  if (m->bf16 && sub_store_enabled()) {
+    for (size_t k = 0; k < p.ops.size(); ++k) {
+      Op& P = p.ops[k];
+      if (P.t != OP_PAIR || P.out.buf < 0 || P.out.ld != P.out.C || P.out.coff != 0) continue;
+      const int buf = P.out.buf;
+      int uses = 0;
+      Op* ds = nullptr;
+      for (size_t q = k + 1; q < p.ops.size(); ++q) {  // (earlier ops may share the buffer: in-place residuals)
+        Op& o = p.ops[q];
+        if (o.t != OP_PACK_IN && o.in.buf == buf) ++uses;
+        if (o.has_res && o.res.buf == buf) ++uses;
+        if (o.dual && o.in2.buf == buf) { ++uses; ds = &o; }
+        if (o.out.buf == buf || (o.t == OP_PAIR && o.out2.buf == buf) || (o.ksplit > 1 && o.ws.buf == buf)) uses += 2;
+      }
+      if (uses != 1 || !ds || ds->t != OP_CONV || (ds->tc_mode != 4 && ds->tc_mode != 5)) continue;
+      const ConvW& wd = m->convs[ds->conv];
+      const int sh = (P.out.H + 1) / 2, sw = (P.out.W + 1) / 2;
+      if (wd.res_identity || wd.stride2 != 2 || ds->in2.coff != 0 || ds->in2.ld != P.out.ld || ds->out.H != sh ||
+          ds->out.W != sw)
+        continue;
+      const View sub = b.compact(P.out.C, sh, sw);
+      P.sub_out = true;
+      P.full_h = P.out.H;
+      P.full_w = P.out.W;
+      P.out = sub;
+      P.bytes -= 0.75 * (double)P.full_h * P.full_w * P.out.C * m->es;
+      P.desc += " (block output stored at stride 2)";
+      ds->in2 = sub;
+      ds->in2_stride = 1;
+    }
+  }
   // liveness + first-fit arena placement (sizes at max_batch)
   for (size_t k = 0; k < p.ops.size(); ++k) {
     const Op& o = p.ops[k];
@@ -1094,7 +1144,10 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       const ConvW& wa = m->convs[o.conv];
       const ConvW& wb = m->convs[o.conv2];
       PairArgs a;
-      a.M = (long long)nb * o.out.H * o.out.W;
+      a.M = o.sub_out ? (long long)nb * o.full_h * o.full_w : (long long)nb * o.out.H * o.out.W;
+      a.y1_sub = o.sub_out ? vptr(m, p, o.out, out) : nullptr;
+      a.H = o.sub_out ? o.full_h : o.out.H;
+      a.W = o.sub_out ? o.full_w : o.out.W;
       a.k1_chunks = wa.K / 64;
       a.k2_diag = wa.res_identity ? 1 : 0;
       a.k2_chunks = wa.res_identity ? 2 : wa.K2 / 64;
@@ -1133,7 +1186,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.nchw = o.nchw_out;
       a.M = (long long)nb * a.OH * a.OW;
       a.k2_chunks = o.dual ? (w.res_identity ? w.bn / 64 : w.K2 / 64) : 0;
-      a.stride2 = w.stride2;
+      a.stride2 = o.in2_stride ? o.in2_stride : w.stride2;
       a.k2_diag = w.res_identity ? 1 : 0;
       if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
         a.C = 64; a.KH = 4; a.KW = 1; a.stride = 1; a.pad = 0;
@@ -1353,7 +1406,7 @@ hapi_status finalize_tmaps(hapi_model* m) {
         if (st != HAPI_OK) return st;
       }
       if (o.dual && o.tc_mode == 5) {
-        if ((st = encode_im2col(m, vptr(m, p, o.in2, nullptr), o.in2, w.cs2, 1, 1, w.stride2, 0, &o.tmap_a2,
+        if ((st = encode_im2col(m, vptr(m, p, o.in2, nullptr), o.in2, w.cs2, 1, 1, o.in2_stride ? o.in2_stride : w.stride2, 0, &o.tmap_a2,
                                 o.desc + " A2 im2col")) != HAPI_OK)
           return st;
       } else if (o.dual) {
@@ -1366,7 +1419,7 @@ hapi_status finalize_tmaps(hapi_model* m) {
           cuuint32_t estr[2] = {1, 1};
           st = encode_bf16(&o.tmap_a2, 2, base2, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " A2");
         } else {
-          const cuuint32_t sd = (cuuint32_t)w.stride2;
+          const cuuint32_t sd = (cuuint32_t)(o.in2_stride ? o.in2_stride : w.stride2);
           cuuint64_t dims[4] = {(cuuint64_t)w.cs2, (cuuint64_t)o.in2.W, (cuuint64_t)o.in2.H, (cuuint64_t)m->d.max_batch};
           cuuint64_t strides[3] = {ld2, ld2 * o.in2.W, ld2 * o.in2.W * o.in2.H};
           cuuint32_t box[4] = {64, (cuuint32_t)o.wb * sd, (cuuint32_t)o.hb * sd, (cuuint32_t)o.nb};

@@ -49,6 +49,8 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("resnet50", 21, 96, 6, "HAPI_DUAL_M", None, "0"),      # two M sub-tiles per weight stage (halo mode)
     ("resnet50", 21, 96, 6, "HAPI_CLUSTER", "1", None),     # 2-CTA multicast weights (opt-in)
     ("resnet50", 21, 160, 3, "HAPI_CLUSTER", "1", None),    # ... odd M-tile count (OOB pair tile)
+    ("resnet50", 21, 96, 6, "HAPI_SUB_STORE", None, "0"),   # pair output stored at stride 2 for the ds
+    ("resnet50", 21, 100, 3, "HAPI_SUB_STORE", None, "0"),  # ... odd 25x25 map (13x13 subsample)
 ])
 def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off):
     fused = _run(tmp_path, {flag: on} if on else {}, arch, split, size, n, "on")
@@ -56,3 +58,21 @@ def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off
     assert fused.shape == plain.shape
     assert np.array_equal(fused.view(np.uint32), plain.view(np.uint32)), (
         flag, int((fused != plain).sum()), float(np.abs(fused - plain).max()))
+
+
+@pytest.mark.gpu
+def test_sub_store_is_planned():
+    """The layer1 -> layer2 transition pair of ResNet-50 stores its block output at stride 2
+    (its only other reader is layer2.0's fused 1x1/s2 downsample); a split at layer1's output
+    (s = 7, the block output is the split layer) keeps the full store."""
+    import paper_2210_08650_b200 as H
+    import hapi_inputs
+    P = list(hapi_inputs.params("resnet50", 1).values())
+    m = H.Model("resnet50", "bf16", P, 2, 7, 21, in_h=96, in_w=96)
+    try:
+        for s in (8, 21):
+            d = m.plan_info(s)["desc"]
+            assert sum("stored at stride 2" in x for x in d) == 1, d
+        assert not any("stored at stride 2" in x for x in m.plan_info(7)["desc"])
+    finally:
+        m.close()
