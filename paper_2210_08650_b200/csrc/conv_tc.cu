@@ -923,16 +923,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const __nv_bfloat16* rb = static_cast<const __nv_bfloat16*>(a.res);
     uint32_t rs = 0, rph = 0;
     int blk = 0;
-    int iter = 0;
+    int iter = 0, bias_tn = -1;
     for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
       const int tn = tile - (tile / g.n_tiles) * g.n_tiles;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
-      // bias of this tile's columns -> smem (the previous tile's readers are past the
-      // last epi_bar of that tile)
-      for (int j = et; j < BN; j += NUM_EPI_THREADS) {
-        const int n = tn * BN + j;
-        sBias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
+      // bias of this tile's columns -> smem, only when the N tile changes (a global load per
+      // tile would put an L2 round trip on every tile of the epilogue-bound small-K convs;
+      // the previous tile's readers are past the last epi_bar of that tile)
+      if (tn != bias_tn) {
+        for (int j = et; j < BN; j += NUM_EPI_THREADS) {
+          const int n = tn * BN + j;
+          sBias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
+        }
+        bias_tn = tn;
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
