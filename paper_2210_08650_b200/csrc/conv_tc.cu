@@ -103,6 +103,7 @@ struct Geo {
   int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
   int mc;                           // 1: 2-CTA cluster, each weight chunk multicast to both CTAs
   int n_pairs;                      // mc: (M-tile pair, N tile) work items
+  int warp_store;                   // 1: each epilogue warp stores its own [32 x 32] boxes (tmap_yw)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -177,7 +178,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const ConvArgs a, const Geo g, const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_y,
                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2,
-                   const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_bh) {
+                   const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_bh,
+                   const __grid_constant__ CUtensorMap tmap_yw) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
   // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
@@ -990,6 +992,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         epi_bar();
+      } else if (!SPATIAL && g.warp_store) {
+        // flat tiles: every warp stages and stores its own [32 rows x 32 cols] boxes (its TMEM
+        // lane quarter x its column half of each SB block), so no CTA-wide barrier sits between
+        // the TMEM drain and the stores; per-warp double buffer of 2 KB (64-byte swizzle)
+        for (int jb = 0; jb < BN; jb += SB) {
+          const int n0 = tn * BN + jb;
+          if (n0 >= a.Cout) break;  // uniform
+          if (g.has_res) mbar_wait(&rfull[rs], rph);
+          const uint32_t rsm = smem_u32(sR + rs * C::SB_BYTES);
+#pragma unroll
+          for (int sub = gsel; sub < SB / 32; sub += 2) {
+            const uint32_t stg = smem_u32(sY) + (uint32_t)(warp * 2 + (blk & 1)) * 2048u;
+            if (lane == 0) bulk_wait_read1();  // this buffer's store (two boxes ago) has read it
+            __syncwarp();
+            uint32_t v[32];
+            tmem_ld32(t_row + jb + sub * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const int chunk = sub * 4 + c4;
+              float f[8];
+              {
+                const uint32_t ba = smem_u32(sBias + jb + chunk * 8);
+                const float4 b0 = lds_f4(ba), b1 = lds_f4(ba + 16);
+                const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = __uint_as_float(v[c4 * 8 + j]) + bb[j];
+              }
+              if (g.has_res) {
+                uint32_t r0, r1, r2, r3;
+                asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                             : "r"(rsm + swz_off<C::SWZ>(row, chunk)));
+                const uint32_t rr[4] = {r0, r1, r2, r3};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const float2 r2f = unpack_bf16x2(rr[j]);
+                  f[2 * j] += r2f.x;
+                  f[2 * j + 1] += r2f.y;
+                }
+              }
+              if (a.relu) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) f[j] = fmaxf(f[j], 0.f);
+              }
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + swz_off<64>(lane, c4)),
+                           "r"(pack_bf16x2(f[0], f[1])), "r"(pack_bf16x2(f[2], f[3])), "r"(pack_bf16x2(f[4], f[5])),
+                           "r"(pack_bf16x2(f[6], f[7]))
+                           : "memory");
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmap_yw, stg, n0 + sub * 32, tm * BM + quarter * 32);
+              bulk_commit();
+            }
+            ++blk;
+          }
+          if (g.has_res) {
+            mbar_arrive(&rempty[rs]);
+            if (++rs == (uint32_t)g.res_depth) { rs = 0; rph ^= 1; }
+          }
+        }
       } else {
         int w0 = 0, h0 = 0, b0 = 0;
         if (SPATIAL) tile_origin(g, tm, &w0, &h0, &b0);
@@ -1067,7 +1132,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
-    if (et == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();  // (per-warp stores: every warp's lane 0 owns bulk groups)
   }
 
   tc_fence_before();
@@ -1090,6 +1155,16 @@ bool bres_enabled() {  // HAPI_BRES=1: also keep weights resident in modes 3/4 (
 
 // 2-CTA weight multicast is correct (parity-tested) but measured neutral-to-slower on
 // ResNet-50 b512 (+1.5%: the weight stream is not the limiter), so it is opt-in: HAPI_CLUSTER=1.
+// Per-warp [32 x 32] epilogue stores for flat (non-spatial) tiles; HAPI_WARP_STORE=0 restores
+// the CTA-wide [128 x SB] staging block (A/B and bitwise tests).
+bool warp_store_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_WARP_STORE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool cluster_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_CLUSTER");
@@ -1183,7 +1258,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   if (!g.mc)
     return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
                       mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b,
-                      mp.b2 ? *mp.b2 : *b, *b);
+                      mp.b2 ? *mp.b2 : *b, *b, mp.yw ? *mp.yw : *b);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -1199,7 +1274,8 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, MODE>, a, g, mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b,
-                            mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b, mp.b2 ? *mp.b2 : *b, *mp.bh);
+                            mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b, mp.b2 ? *mp.b2 : *b, *mp.bh,
+                            mp.yw ? *mp.yw : *b);
 }
 
 template <int BN>
@@ -1352,6 +1428,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   }
   if ((mode == 3 || mode == 4 || mode == 5 || mode == 6 || mode == 8) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
   if (g.tma_out && !mp.y) return cudaErrorInvalidValue;
+  g.warp_store = (g.tma_out && mp.yw && (mode == 3 || mode == 5 || mode == 7) && warp_store_enabled()) ? 1 : 0;
   if (g.has_res && g.tma_out && !mp.r) return cudaErrorInvalidValue;
   if (g.has_res && !g.tma_out) g.has_res = 0;  // NCHW path reads the residual directly
   switch (bn) {

@@ -97,6 +97,7 @@ struct ConvMaps {
   const CUtensorMap* bh; // weights with a {64, bn/2} box (2-CTA multicast halves) or nullptr
   const CUtensorMap* y;  // output view (NHWC epilogue via TMA store) or nullptr for NCHW
   const CUtensorMap* r;  // residual view or nullptr
+  const CUtensorMap* yw; // output view with a {32, 32} box, 64B swizzle (per-warp epilogue stores) or nullptr
 };
 // Chained 1x1 pair (conv_pair.cu): a bottleneck's conv3 (+ residual as second A source) and
 // the next block's conv1 per 128-row tile; the block output tile stays in smem as conv1's A.

@@ -188,6 +188,8 @@ struct Op {
   CUtensorMap tmap_a;            // modes 3/4 (built after the arena is placed)
   CUtensorMap tmap_y;            // NHWC output view (TMA-store epilogue)
   CUtensorMap tmap_r;            // residual view
+  CUtensorMap tmap_yw;           // NHWC output view with a {32, 32} box (per-warp epilogue stores)
+  bool has_yw = false;
   bool dual = false;             // second A source (fused downsample) = in2
   View in2;
   CUtensorMap tmap_a2;
@@ -1205,6 +1207,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
         mp.bh = w.has_half ? &w.tmap_half : nullptr;
         mp.y = o.nchw_out ? nullptr : &o.tmap_y;
         mp.r = (o.has_res && !o.nchw_out) ? &o.tmap_r : nullptr;
+        mp.yw = o.has_yw ? &o.tmap_yw : nullptr;
         e = conv_tc_launch(a, mp, o.tc_mode == 8 ? 128 : w.bn, o.tc_mode, o.wb, o.hb, o.nb, m->num_sms, st);
       } else {
         a.ksplit = o.ksplit;
@@ -1431,6 +1434,18 @@ hapi_status finalize_tmaps(hapi_model* m) {
       if (!o.nchw_out && o.tc_mode != 8) {
         const int cols = conv_tc_store_cols(w.bn);
         if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y")) != HAPI_OK) return st;
+        if (o.t == OP_CONV && (o.tc_mode == 3 || o.tc_mode == 5 || o.tc_mode == 7)) {
+          // flat output tiles: per-warp [32 rows x 32 channels] store boxes
+          void* base = vptr(m, p, o.out, nullptr);
+          cuuint64_t dims[2] = {(cuuint64_t)o.out.C, (cuuint64_t)m->d.max_batch * o.out.H * o.out.W};
+          cuuint64_t strides[1] = {(cuuint64_t)o.out.ld * 2};
+          cuuint32_t box[2] = {32, 32};
+          cuuint32_t estr[2] = {1, 1};
+          if ((st = encode_bf16(&o.tmap_yw, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_64B,
+                                o.desc + " Yw")) != HAPI_OK)
+            return st;
+          o.has_yw = true;
+        }
         if (o.has_res && (st = encode_view(m, p, o, o.res, cols, &o.tmap_r, "R")) != HAPI_OK) return st;
       }
     }
