@@ -46,6 +46,9 @@ constexpr int P_STG_BYTES = PM * 64 * 2; // one [128 x 64] bf16 block, 16 KB
 constexpr int P_MAX_BIAS1 = 512;
 constexpr int P_TMEM_ACC2 = 2 * BN1;     // GEMM2 accumulator column base
 
+// named barrier of the two epilogue warps (q, q + 4) that share TMEM lane quarter q
+__device__ __forceinline__ void quarter_bar(int q) { asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory"); }
+
 template <int N2>
 struct PairCfg {
   static constexpr int STAGE = P_A_BYTES + BN1 * PK * 2;  // GEMM1 ring: A chunk + W3 chunk
@@ -241,6 +244,7 @@ __global__ void __launch_bounds__(P_THREADS, 1)
     const int quarter = warp & 3, gsel = warp >> 2;
     const int row = quarter * 32 + lane;
     const int et = threadIdx.x;
+    const bool lead = gsel == 0 && lane == 0;  // issues (and waits for) its row quarter's stores
     for (int i = et; i < a.cout1; i += P_EPI_THREADS) sBias1[i] = a.bias1 ? __ldg(a.bias1 + i) : 0.f;
     for (int i = et; i < N2; i += P_EPI_THREADS) sBias2[i] = a.bias2 ? __ldg(a.bias2 + i) : 0.f;
     epi_bar();
@@ -270,10 +274,12 @@ __global__ void __launch_bounds__(P_THREADS, 1)
         // staging pair `buf` was last read by GEMM2(n-2) and by the TMA stores of n-2 (and,
         // for the first N tile of a row tile, by the previous tile's GEMM2-output stores)
         mbar_wait(&a2empty[buf], ((n >> 1) & 1) ^ 1);
-        if (et == 0) {
+        // warps q and q+4 own rows 32q..32q+31 of every staging block (and store exactly those
+        // rows), so a 64-thread barrier per row quarter replaces the CTA-wide one
+        if (lead) {
           if (j == 0) bulk_wait_read0(); else bulk_wait_read1();
         }
-        epi_bar();
+        quarter_bar(quarter);
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           uint32_t v[32];
@@ -301,11 +307,12 @@ __global__ void __launch_bounds__(P_THREADS, 1)
         mbar_arrive(&tempty1[buf]);
         fence_proxy_async_smem();
         mbar_arrive(&a2full[buf]);
-        epi_bar();
-        if (et == 0) {
+        quarter_bar(quarter);
+        if (lead) {
           if (!a.y1_sub)
             for (int b = 0; b < 2; ++b)
-              tma_store_2d(&tm_y1, stg0 + (buf * 2 + b) * P_STG_BYTES, j * BN1 + b * 64, row0);
+              tma_store_2d(&tm_y1, stg0 + (buf * 2 + b) * P_STG_BYTES + quarter * 32 * 128, j * BN1 + b * 64,
+                           row0 + quarter * 32);
           bulk_commit();
         }
       }
@@ -313,8 +320,8 @@ __global__ void __launch_bounds__(P_THREADS, 1)
       // GEMM2 of this tile has completed -- tfull2 -- so only the store reads are pending)
       mbar_wait(tfull2, it & 1);
       tc_fence_after();
-      if (et == 0) bulk_wait_read0();
-      epi_bar();
+      if (lead) bulk_wait_read0();
+      quarter_bar(quarter);
 #pragma unroll
       for (int b = 0; b < N2 / 64; ++b) {
         uint32_t v[32];
@@ -339,13 +346,14 @@ __global__ void __launch_bounds__(P_THREADS, 1)
       tc_fence_before();
       mbar_arrive(tempty2);
       fence_proxy_async_smem();
-      epi_bar();
-      if (et == 0) {
-        for (int b = 0; b < N2 / 64; ++b) tma_store_2d(&tm_y2, stg0 + b * P_STG_BYTES, b * 64, row0);
+      quarter_bar(quarter);
+      if (lead) {
+        for (int b = 0; b < N2 / 64; ++b)
+          tma_store_2d(&tm_y2, stg0 + b * P_STG_BYTES + quarter * 32 * 128, b * 64, row0 + quarter * 32);
         bulk_commit();
       }
     }
-    if (et == 0) bulk_wait_all();
+    if (lead) bulk_wait_all();
   }
 
   tc_fence_before();

@@ -119,8 +119,8 @@ struct PairMaps {
   const CUtensorMap* b1;  // conv3 weights [cout1][Kp], box {64, 128}
   const CUtensorMap* id;  // 64x64 identity block, box {64, 128}, loaded at row -64c
   const CUtensorMap* b2;  // next conv1 weights [n2][cout1], box {64, n2}
-  const CUtensorMap* y1;  // block output view [M][cout1], box {64, 128}, 128B swizzle
-  const CUtensorMap* y2;  // next conv1 output view [M][n2], box {64, 128}, 128B swizzle
+  const CUtensorMap* y1;  // block output view [M][cout1], box {64, 32} (one row quarter), 128B swizzle
+  const CUtensorMap* y2;  // next conv1 output view [M][n2], box {64, 32}, 128B swizzle
 };
 cudaError_t conv_pair_launch(const PairArgs& a, const PairMaps& mp, int n2, int num_sms, cudaStream_t st);
 

@@ -1305,7 +1305,7 @@ hapi_status encode_im2col(hapi_model* m, void* base, const View& v, int C, int k
 // {cols, 128} box for linear tiles, 4D {C, W, H, N} with a {cols, wb, hb, nb} box for
 // mode-4 spatial tiles.  The batch extent is max_batch.
 hapi_status encode_view(hapi_model* m, const Plan& p, const Op& o, const View& v, int cols, CUtensorMap* map,
-                        const char* what) {
+                        const char* what, int rows = 128) {
   const cuuint64_t es = 2, ld = (cuuint64_t)v.ld;
   const CUtensorMapSwizzle swz = cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   void* base = vptr(m, p, v, nullptr);
@@ -1318,7 +1318,7 @@ hapi_status encode_view(hapi_model* m, const Plan& p, const Op& o, const View& v
   }
   cuuint64_t dims[2] = {(cuuint64_t)v.C, (cuuint64_t)m->d.max_batch * v.H * v.W};
   cuuint64_t strides[1] = {ld * es};
-  cuuint32_t box[2] = {(cuuint32_t)cols, 128};
+  cuuint32_t box[2] = {(cuuint32_t)cols, (cuuint32_t)rows};
   cuuint32_t estr[2] = {1, 1};
   return encode_bf16(map, 2, base, dims, strides, box, estr, swz, o.desc + " " + what);
 }
@@ -1346,7 +1346,8 @@ hapi_status finalize_tmaps(hapi_model* m) {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return set_error(HAPI_ERR_CUDA, "pair weight tensor map failed (%d)", (int)r);
-        if ((st = encode_view(m, p, o, o.out2, 64, &o.tmap_y2, "Y2")) != HAPI_OK) return st;
+        // the pair kernel stores one 32-row quarter of a [128 x 64] staging block per box
+        if ((st = encode_view(m, p, o, o.out2, 64, &o.tmap_y2, "Y2", 32)) != HAPI_OK) return st;
       }
       if (o.tc_mode == 8) {
         // stem+pool boxes over the padded s2d input [N][HP][WP][16] as a 5D view
@@ -1433,7 +1434,7 @@ hapi_status finalize_tmaps(hapi_model* m) {
       }
       if (!o.nchw_out && o.tc_mode != 8) {
         const int cols = conv_tc_store_cols(w.bn);
-        if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y")) != HAPI_OK) return st;
+        if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y", o.t == OP_PAIR ? 32 : 128)) != HAPI_OK) return st;
         if (o.t == OP_CONV && (o.tc_mode == 3 || o.tc_mode == 5 || o.tc_mode == 7)) {
           // flat output tiles: per-warp [32 rows x 32 channels] store boxes
           void* base = vptr(m, p, o.out, nullptr);
