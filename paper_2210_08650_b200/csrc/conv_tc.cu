@@ -103,7 +103,6 @@ struct Geo {
   int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
   int mc;                           // 1: 2-CTA cluster, each weight chunk multicast to both CTAs
   int n_pairs;                      // mc: (M-tile pair, N tile) work items
-  int warp_store;                   // 1: each epilogue warp stores its own [32 x 32] boxes (tmap_yw)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -178,8 +177,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     conv_tc_kernel(const ConvArgs a, const Geo g, const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const __grid_constant__ CUtensorMap tmap_y,
                    const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_a2,
-                   const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_bh,
-                   const __grid_constant__ CUtensorMap tmap_yw) {
+                   const __grid_constant__ CUtensorMap tmap_b2, const __grid_constant__ CUtensorMap tmap_bh) {
   using C = Cfg<BN>;
   constexpr int SB = C::SB;
   // MODE 9 = halo mode 6 with two M sub-tiles per B stage (g.mode stays 6 for the geometry)
@@ -189,6 +187,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr int MT = (MODE == 9 || MODE == 10) ? 2 : 1;
   constexpr bool TMA_A = (MODE == 3 || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
+  // 1x1 TMA tiles (mode 3): the epilogue stores per-warp [32 x 32] boxes through the 7th map
+  // (tmap_bh, free in mode 3: no multicast there); the CTA-wide staging path is compiled only
+  // into the other modes.  (Measured: -3..-5% on the epilogue-bound 1x1 convs.  Tried on the
+  // im2col modes too: +7..9% on the MMA-bound 3x3 convs, so they keep the staging block.)
+  constexpr bool WARP_STORE = (MODE == 3);
   const int S = g.stages;
   const int AS = (HALO || MODE == 8) ? g.a_stages : S;
   constexpr int CPS = (MODE == 3 && BN <= 128) ? 2 : 1;  // == g.cps (host); mode 4 measured better at 1
@@ -934,10 +937,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       // tile would put an L2 round trip on every tile of the epilogue-bound small-K convs;
       // the previous tile's readers are past the last epi_bar of that tile)
       if (tn != bias_tn) {
+        // (the per-warp store path has no CTA-wide barrier of its own: fence the table here)
+        if constexpr (WARP_STORE) epi_bar();
         for (int j = et; j < BN; j += NUM_EPI_THREADS) {
           const int n = tn * BN + j;
           sBias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
         }
+        if constexpr (WARP_STORE) epi_bar();
         bias_tn = tn;
       }
       mbar_wait(&tfull[acc], acc_phase);
@@ -992,7 +998,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         epi_bar();
-      } else if (!SPATIAL && g.warp_store) {
+      } else if constexpr (WARP_STORE) {
         // flat tiles: every warp stages and stores its own [32 rows x 32 cols] boxes (its TMEM
         // lane quarter x its column half of each SB block), so no CTA-wide barrier sits between
         // the TMEM drain and the stores; per-warp double buffer of 2 KB (64-byte swizzle)
@@ -1045,7 +1051,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmap_yw, stg, n0 + sub * 32, tm * BM + quarter * 32);
+              tma_store_2d(&tmap_bh, stg, n0 + sub * 32, tm * BM + quarter * 32);
               bulk_commit();
             }
             ++blk;
@@ -1132,7 +1138,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
-    if (lane == 0) bulk_wait_all();  // (per-warp stores: every warp's lane 0 owns bulk groups)
+    if (WARP_STORE ? lane == 0 : et == 0) bulk_wait_all();  // (per-warp stores: each warp's lane 0 owns groups)
   }
 
   tc_fence_before();
@@ -1155,16 +1161,6 @@ bool bres_enabled() {  // HAPI_BRES=1: also keep weights resident in modes 3/4 (
 
 // 2-CTA weight multicast is correct (parity-tested) but measured neutral-to-slower on
 // ResNet-50 b512 (+1.5%: the weight stream is not the limiter), so it is opt-in: HAPI_CLUSTER=1.
-// Per-warp [32 x 32] epilogue stores for flat (non-spatial) tiles; HAPI_WARP_STORE=0 restores
-// the CTA-wide [128 x SB] staging block (A/B and bitwise tests).
-bool warp_store_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("HAPI_WARP_STORE");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
-
 bool cluster_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_CLUSTER");
@@ -1245,7 +1241,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   // resident), no identity block, at least two M tiles; every weight chunk then crosses L2
   // once per CTA pair instead of once per CTA
   g.mc = 0;
-  if ((g.mode == 3 || g.mode == 4 || g.mode == 5) && g.mt == 1 && !g.b_res && !a.k2_diag && BN >= 128 && mp.bh &&
+  if ((g.mode == 4 || g.mode == 5) && g.mt == 1 && !g.b_res && !a.k2_diag && BN >= 128 && mp.bh &&
       g.m_tiles >= 2 && cluster_enabled()) {
     g.mc = 1;
     g.n_pairs = (g.m_tiles + 1) / 2 * g.n_tiles;
@@ -1258,7 +1254,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   if (!g.mc)
     return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
                       mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b,
-                      mp.b2 ? *mp.b2 : *b, *b, mp.yw ? *mp.yw : *b);
+                      mp.b2 ? *mp.b2 : *b, (MODE == 3 && mp.yw) ? *mp.yw : *b);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -1274,8 +1270,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, conv_tc_kernel<BN, MODE>, a, g, mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b,
-                            mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b, mp.b2 ? *mp.b2 : *b, *mp.bh,
-                            mp.yw ? *mp.yw : *b);
+                            mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b, mp.b2 ? *mp.b2 : *b, *mp.bh);
 }
 
 template <int BN>
@@ -1428,7 +1423,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   }
   if ((mode == 3 || mode == 4 || mode == 5 || mode == 6 || mode == 8) && (!mp.a || a.C % BK != 0)) return cudaErrorInvalidValue;
   if (g.tma_out && !mp.y) return cudaErrorInvalidValue;
-  g.warp_store = (g.tma_out && mp.yw && (mode == 3 || mode == 5 || mode == 7) && warp_store_enabled()) ? 1 : 0;
+  if (g.tma_out && mode == 3 && !mp.yw) return cudaErrorInvalidValue;  // per-warp store map
   if (g.has_res && g.tma_out && !mp.r) return cudaErrorInvalidValue;
   if (g.has_res && !g.tma_out) g.has_res = 0;  // NCHW path reads the residual directly
   switch (bn) {

@@ -1435,8 +1435,8 @@ hapi_status finalize_tmaps(hapi_model* m) {
       if (!o.nchw_out && o.tc_mode != 8) {
         const int cols = conv_tc_store_cols(w.bn);
         if ((st = encode_view(m, p, o, o.out, cols, &o.tmap_y, "Y", o.t == OP_PAIR ? 32 : 128)) != HAPI_OK) return st;
-        if (o.t == OP_CONV && (o.tc_mode == 3 || o.tc_mode == 5 || o.tc_mode == 7)) {
-          // flat output tiles: per-warp [32 rows x 32 channels] store boxes
+        if (o.t == OP_CONV && o.tc_mode == 3) {
+          // 1x1 tiles: per-warp [32 rows x 32 channels] store boxes
           void* base = vptr(m, p, o.out, nullptr);
           cuuint64_t dims[2] = {(cuuint64_t)o.out.C, (cuuint64_t)m->d.max_batch * o.out.H * o.out.W};
           cuuint64_t strides[1] = {(cuuint64_t)o.out.ld * 2};
