@@ -150,12 +150,13 @@ def test_chunking_batch_shard_invariance_determinism(act):
     np.testing.assert_array_equal(np.concatenate(shards), full)
 
 
-def test_host_path_equals_device_path():
+@pytest.mark.parametrize("n,max_batch", [(9, 4), (200, 64)])   # (200, 64): ramped chunks 32, 64, 64, 40
+def test_host_path_equals_device_path(n, max_batch):
     H = _H()
-    arch, s, n = "resnet18", 10, 9
+    arch, s = "resnet18", 10
     P = hapi_inputs.params(arch, 10)
     x = hapi_inputs.images(n, 11, 64, 64)
-    m = H.Model(arch, "bf16", list(P.values()), 4, s, s, in_h=64, in_w=64)
+    m = H.Model(arch, "bf16", list(P.values()), max_batch, s, s, in_h=64, in_w=64)
     dev, _ = gpu_forward(arch, "bf16", s, x, P, model=m)
     host, _ = gpu_forward(arch, "bf16", s, x, P, model=m, host=True)
     np.testing.assert_array_equal(dev, host)
