@@ -100,6 +100,29 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
     }
     return;
   }
+  if (layout == 3) {
+    // 3x3/s1/p1 stem on a 3-channel image (VGG): NHWC padded to 8 channels with a zero border
+    // (one row above and below, one column left, wp - W - 1 right), so the stem reads each
+    // filter row as one 8-pixel x 8-channel window (64 contiguous bf16) starting at padded
+    // column ow: one thread per padded pixel of the (H+2) x wp grid
+    const int HP = H + 2, WP = wp;
+    const long long total = (long long)N * HP * WP;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+      const long long n = t / (HP * WP);
+      const int rem = (int)(t - n * HP * WP);
+      const int i = rem / WP - 1, j = rem - (rem / WP) * WP - 1;
+      float v[3] = {0.f, 0.f, 0.f};
+      if (i >= 0 && i < H && j >= 0 && j < W) {
+        const float* src = img + n * 3 * HW + (long long)i * W + j;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c] = __ldg(src + c * HW);
+      }
+      uint4 o;
+      o.x = pack2(v[0], v[1]); o.y = pack2(v[2], 0.f); o.z = 0u; o.w = 0u;
+      reinterpret_cast<uint4*>(y)[t] = o;
+    }
+    return;
+  }
   const long long total = (long long)N * HW;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long n = i / HW;
@@ -317,7 +340,8 @@ cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int
 }
 
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, int wp, cudaStream_t st) {
-  const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * wp : (long long)N * H * W;
+  const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * wp
+                          : layout == 3 ? (long long)N * (H + 2) * wp : (long long)N * H * W;
   launch_pdl(pack_input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, img, y, N, H, W, layout, wp);
   return cudaGetLastError();
 }

@@ -111,6 +111,14 @@ bool pair_enabled() {
   return on;
 }
 
+bool win3_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_WIN3");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool sub_store_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_SUB_STORE");
@@ -329,6 +337,8 @@ struct ConvSpec {
   int fh = 0, fw = 0;    // linear on a flattened (cin/(fh*fw), fh, fw) map: permute columns
   bool linear = false;
   bool s2d = false;      // 7x7/s2/p3 stem re-expressed as 4x4/s1/p2 on a 2x2 space-to-depth input
+  bool win3 = false;     // 3x3/s1/p1 stem on 3 channels (VGG) over the zero-bordered 8-channel input,
+                         // each filter row one 8-pixel x 8-channel window: stored as KH=3, KW=8, C=8
   // fused downsample (bf16): out = conv(x1) + ds(x2) with ds a 1x1/stride2 conv + folded BN,
   // packed as extra K columns after the first conv's
   std::string w2name, fold2;
@@ -340,7 +350,8 @@ struct ConvSpec {
 
 hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   std::string key = s.wname + "|" + s.bname + "|" + s.fold_bn + "|" + s.pro_bn + "|" + std::to_string(s.cs) + "|" +
-                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "") + "|" + s.w2name + "|" +
+                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "") + (s.win3 ? "|win3" : "") + "|" +
+                    s.w2name + "|" +
                     s.fold2 + (s.res_identity ? "|resid" : "");
   auto it = m->conv_index.find(key);
   if (it != m->conv_index.end()) {
@@ -370,8 +381,9 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   cw.cs = s.cs;
   cw.cout = s.cout;
   cw.kh = cw.kw = s.s2d ? 4 : kk;
+  if (s.win3) cw.kw = 8;
   cw.stride = s.s2d ? 1 : s.stride;
-  cw.pad = s.s2d ? 2 : s.pad;
+  cw.pad = s.s2d ? 2 : (s.win3 ? 0 : s.pad);
   cw.K = cw.kh * cw.kw * s.cs;
   cw.real_flops_per_px = 2.0 * ((double)kk * kk * s.cin + s.cin2) * s.cout;
   cw.K2 = w2 ? s.cin2 : 0;
@@ -395,6 +407,13 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
       const int orr = 2 * r + aa - 1, ott = 2 * t + bb - 1;
       if (orr < 0 || orr >= kk || ott < 0 || ott >= kk) return 0.0;
       double v = w[(((int64_t)o * s.cin + ch) * kk + orr) * kk + ott];
+      if (!fs.empty()) v *= fs[o];
+      return v;
+    }
+    if (s.win3) {
+      // window pixel t of filter row r: original tap (r, t) for t < 3, channel c < 3
+      if (t >= kk || c >= s.cin) return 0.0;
+      double v = w[(((int64_t)o * s.cin + c) * kk + r) * kk + t];
       if (!fs.empty()) v *= fs[o];
       return v;
     }
@@ -581,9 +600,10 @@ struct Builder {
           conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
           o.tc_mode = 4;
         }
-      } else if (cs.s2d) {
+      } else if (cs.s2d || cs.win3) {
         // space-to-depth stem (4x4/s1 over 16-channel pixels): read as a window view whose
-        // rows are 4 adjacent padded pixels (128 B), W stride 32 B -> KH=4, KW=1, C=64 mode 4
+        // rows are 4 adjacent padded pixels (128 B), W stride 32 B -> KH=4, KW=1, C=64 mode 4;
+        // the VGG 3x3 stem likewise: rows of 8 padded 8-channel pixels, W stride 16 B, KH=3
         conv_tc_spatial_tile(out.H, out.W, (int)m->d.max_batch, &o.wb, &o.hb, &o.nb);
         o.tc_mode = 4;
         o.s2d_view = true;
@@ -665,14 +685,18 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   const int start = (int)m->start;
   const bool s2d = start == 0 && m->bf16 && m0.kind == MK_CONV && m0.k == 7 && m0.stride == 2 && m0.pad == 3 &&
                    m0.cin == 3 && H0 % 2 == 0 && W0 % 2 == 0;
-  const int layout = !m->bf16 ? 0 : (s2d ? 2 : 1);
+  const bool win3 = start == 0 && m->bf16 && m0.kind == MK_CONV && m0.k == 3 && m0.stride == 1 && m0.pad == 1 &&
+                    m0.cin == 3 && win3_enabled();
+  const int layout = !m->bf16 ? 0 : (s2d ? 2 : (win3 ? 3 : 1));
   View cur;
   if (start == 0) {
     // s2d padded width: 3 zero columns on the left, >= 1 on the right, and room for the
     // stem+pool kernel's last strip box (S strips of 2 pq stem columns, box width 2 pq + 4)
     const int sw = W0 / 2, spw = (sw - 1) / 2 + 1, sS = (spw + 29) / 30, spq = (spw + sS - 1) / sS;
     const int WP = std::max(sw, 2 * sS * spq) + 4;
-    cur = layout == 2 ? b.compact(16, H0 / 2 + 3, WP) : b.compact(layout == 1 ? 8 : 3, H0, W0);
+    cur = layout == 2   ? b.compact(16, H0 / 2 + 3, WP)
+          : layout == 3 ? b.compact(8, H0 + 2, W0 + 8)
+                        : b.compact(layout == 1 ? 8 : 3, H0, W0);
     Op o;
     o.t = OP_PACK_IN;
     o.out = cur;
@@ -715,7 +739,8 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         cs.cin = md.cin; cs.cout = md.cout; cs.k = md.k; cs.stride = md.stride; cs.pad = md.pad;
         cs.cs = cur.C;
         cs.s2d = (i == 0 && s2d);
-        const int ih = cs.s2d ? H0 : cur.H, iw = cs.s2d ? W0 : cur.W;
+        cs.win3 = (i == 0 && win3);
+        const int ih = (cs.s2d || cs.win3) ? H0 : cur.H, iw = (cs.s2d || cs.win3) ? W0 : cur.W;
         const int oh = out_dim(ih, md.k, md.stride, md.pad), ow = out_dim(iw, md.k, md.stride, md.pad);
         const int jp = j + (relu ? 1 : 0);
         if (cs.s2d && relu && md.cout <= 64 && jp < split && mods[jp].kind == MK_MAXPOOL && mods[jp].k == 3 &&
@@ -1191,7 +1216,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.stride2 = o.in2_stride ? o.in2_stride : w.stride2;
       a.k2_diag = w.res_identity ? 1 : 0;
       if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
-        a.C = 64; a.KH = 4; a.KW = 1; a.stride = 1; a.pad = 0;
+        a.C = 64; a.KH = w.kh; a.KW = 1; a.stride = 1; a.pad = 0;
       }
       if (o.tc_mode == 8) {  // the kernel iterates the stem map; y is the pooled map
         a.OH = o.conv_oh; a.OW = o.conv_ow;
@@ -1367,8 +1392,11 @@ hapi_status finalize_tmaps(hapi_model* m) {
         // overlapping window view of the padded s2d input: element (e, w, h, n) at
         // base + n*HP*WP*32 + h*WP*32 + (w+1)*32 + 2e, e < 64 spans 4 adjacent pixels (stem
         // column w starts at padded column w+1: the buffer has 3 zero columns on the left)
-        void* base = static_cast<char*>(vptr(m, p, o.in, nullptr)) + o.in.ld * 2;
-        const cuuint64_t px = (cuuint64_t)o.in.ld * 2;  // 32 B
+        // (the VGG 3x3 window view, KW = 8: 8-channel pixels, 16 B, and output column w starts
+        // at padded column w -- one zero column on the left)
+        const bool win3 = w.kw == 8;
+        void* base = static_cast<char*>(vptr(m, p, o.in, nullptr)) + (win3 ? 0 : o.in.ld * 2);
+        const cuuint64_t px = (cuuint64_t)o.in.ld * 2;  // 32 B (s2d) / 16 B (win3)
         const int stem_w = o.tc_mode == 8 ? o.conv_ow : o.out.W;
         cuuint64_t dims[4] = {64, (cuuint64_t)stem_w, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
         cuuint64_t strides[3] = {px, px * o.in.W, px * o.in.W * o.in.H};

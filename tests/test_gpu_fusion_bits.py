@@ -76,3 +76,16 @@ def test_sub_store_is_planned():
         assert not any("stored at stride 2" in x for x in m.plan_info(7)["desc"])
     finally:
         m.close()
+
+
+@pytest.mark.gpu
+def test_vgg_window_stem_matches_gather_stem(tmp_path):
+    """The VGG 3x3 stem through the 8-pixel window view (K = 3 rows x 64, zero weights for the
+    window's pixels 3..7) groups the same nonzero products into different K=16 MMA steps than
+    the per-tap gather stem (K = 9 taps x 8 channels), so fp32 rounding differs: equal within
+    a few bf16 ulps, not bitwise (both are checked against the oracle in test_gpu_parity)."""
+    fused = _run(tmp_path, {}, "vgg11", 3, 72, 3, "on")
+    plain = _run(tmp_path, {"HAPI_WIN3": "0"}, "vgg11", 3, 72, 3, "off")
+    a, b = fused.astype(np.float64).ravel(), plain.astype(np.float64).ravel()
+    assert np.linalg.norm(a - b) <= 4e-3 * np.linalg.norm(b)
+
