@@ -103,6 +103,8 @@ struct Geo {
   int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
   int mc;                           // 1: 2-CTA cluster, each weight chunk multicast to both CTAs
   int n_pairs;                      // mc: (M-tile pair, N tile) work items
+  int pool2;                        // mode 4, hb = 2 tiles: 2x2/s2 maxpool fused into the epilogue
+                                    // (y is the pooled map; only pooled pixels reach HBM)
 };
 
 // Row i (0..127) of m-tile tm -> output pixel index m, or -1 when the row is padding.
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], NUM_EPI_THREADS);
+      mbar_init(&tempty[i], (MODE == 4 && g.pool2) ? NUM_EPI_THREADS / 2 : NUM_EPI_THREADS);
     }
     for (int i = 0; i < MAX_RES; ++i) {
       mbar_init(&rfull[i], 1);
@@ -929,7 +931,76 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t rs = 0, rph = 0;
     int blk = 0;
     int iter = 0, bias_tn = -1;
-    for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
+    if (MODE == 4 && g.pool2) {
+      // conv + 2x2/s2 maxpool, [2 x wb] tiles, one N tile (host-checked): the per-tile epilogue is
+      // a latency chain (TMEM drain -> staging -> pooled stores) far longer than the tile's
+      // K = 192 MMAs, so two groups of 4 warps (each covering all four TMEM lane quarters and
+      // all BN columns) take alternate tiles = alternate accumulator buffers, with their own
+      // staging block and named barrier, and the two chains overlap.
+      for (int j = et; j < BN; j += NUM_EPI_THREADS) sBias[j] = (a.bias && j < a.Cout) ? __ldg(a.bias + j) : 0.f;
+      epi_bar();
+      const int grp = gsel, eg = et & 127;
+      const uint32_t stg = smem_u32(sY + grp * C::SB_BYTES);
+      const int pq = g.wb >> 1, nchunk = BN / 8, PW = a.OW >> 1;
+      __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(a.y);
+      for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
+        const int acc = iter & 1;
+        if (acc != grp) continue;
+        mbar_wait(&tfull[acc], (iter >> 1) & 1);
+        tc_fence_after();
+        int w0 = 0, h0 = 0, b0 = 0;
+        tile_origin(g, tile / g.n_tiles, &w0, &h0, &b0);
+        const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll
+        for (int sub = 0; sub < BN / 32; ++sub) {
+          uint32_t v[32];
+          tmem_ld32(t_row + sub * 32, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {
+            const int chunk = sub * 4 + c4;
+            const uint32_t ba = smem_u32(sBias + chunk * 8);
+            const float4 b0v = lds_f4(ba), b1v = lds_f4(ba + 16);
+            const float bb[8] = {b0v.x, b0v.y, b0v.z, b0v.w, b1v.x, b1v.y, b1v.z, b1v.w};
+            float f[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              f[j] = __uint_as_float(v[c4 * 8 + j]) + bb[j];
+              if (a.relu) f[j] = fmaxf(f[j], 0.f);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(stg + swz_off<C::SWZ>(row, chunk)),
+                         "r"(pack_bf16x2(f[0], f[1])), "r"(pack_bf16x2(f[2], f[3])), "r"(pack_bf16x2(f[4], f[5])),
+                         "r"(pack_bf16x2(f[6], f[7]))
+                         : "memory");
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        asm volatile("bar.sync %0, 128;" ::"r"(3 + grp) : "memory");  // the group's staging is complete
+        for (int it = eg; it < pq * nchunk; it += NUM_EPI_THREADS / 2) {
+          const int q = it / nchunk, c = it - q * nchunk;
+          uint32_t r[4][4];
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            const int srow_d = (d >> 1) * g.wb + 2 * q + (d & 1);
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(r[d][0]), "=r"(r[d][1]), "=r"(r[d][2]), "=r"(r[d][3])
+                         : "r"(stg + swz_off<C::SWZ>(srow_d, c)));
+          }
+          uint4 o;
+          o.x = bf16x2_max(bf16x2_max(r[0][0], r[1][0]), bf16x2_max(r[2][0], r[3][0]));
+          o.y = bf16x2_max(bf16x2_max(r[0][1], r[1][1]), bf16x2_max(r[2][1], r[3][1]));
+          o.z = bf16x2_max(bf16x2_max(r[0][2], r[1][2]), bf16x2_max(r[2][2], r[3][2]));
+          o.w = bf16x2_max(bf16x2_max(r[0][3], r[1][3]), bf16x2_max(r[2][3], r[3][3]));
+          const long long pix = ((long long)b0 * (a.OH >> 1) + (h0 >> 1)) * PW + (w0 >> 1) + q;
+          *reinterpret_cast<uint4*>(yp + pix * a.y_ld + c * 8) = o;
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(3 + grp) : "memory");  // staging reads done
+      }
+      iter = -1;  // (the generic loop below is skipped)
+    }
+    for (int k_ = 0, tile = (iter < 0 ? -1 : tile_at(g, 0, num_tiles)); tile >= 0;
+         tile = tile_at(g, ++k_, num_tiles), ++iter) {
       const int tn = tile - (tile / g.n_tiles) * g.n_tiles;
       const int acc = iter & 1;
       const uint32_t acc_phase = (iter >> 1) & 1;
@@ -1394,6 +1465,12 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
       if (bn == 128 && g.n_tiles == 1 && !a.res && need <= SMEM_LIMIT && dual_m_enabled()) g.mt = 2;
     }
   } else if (mode == 4) {
+    if (a.pool2) {
+      if (hb != 2 || nb != 1 || (wb & 1) || a.OW % wb != 0 || (a.OH & 1) || a.res || a.nchw || a.y_ld % 8 != 0 ||
+          a.k2_chunks > 0 || bn > 64 || a.Cout != bn)
+        return cudaErrorInvalidValue;
+      g.pool2 = 1;
+    }
     g.wb = wb; g.hb = hb; g.nb = nb;
     g.tiles_w = (a.OW + wb - 1) / wb;
     g.tiles_h = (a.OH + hb - 1) / hb;

@@ -80,6 +80,9 @@ struct ConvArgs {
   // with the bias / residual / ReLU epilogue
   int ksplit;
   float* ws;
+  // mode 4 with [2 x wb] tiles (wb even, OW % wb == 0, OH even): a 2x2/s2 maxpool follows the
+  // conv and is fused into the epilogue; y / y_ld describe the pooled [N][OH/2][OW/2] map
+  int pool2;
 };
 
 // tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).  A-operand modes:

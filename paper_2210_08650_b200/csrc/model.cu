@@ -214,6 +214,7 @@ struct Op {
   // in2_stride = 1
   bool sub_out = false;
   int full_h = 0, full_w = 0;
+  bool pool2 = false;            // mode-4 conv with the following 2x2/s2 maxpool in its epilogue (out = pooled)
   int in2_stride = 0;            // 0: the conv's own stride2
 };
 
@@ -763,6 +764,32 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           i = jp + 1;
           break;
         }
+        if (cs.win3 && relu && jp < split && mods[jp].kind == MK_MAXPOOL && mods[jp].k == 2 && mods[jp].stride == 2 &&
+            mods[jp].pad == 0 && oh % 2 == 0 && ow % 2 == 0 && stem_pool_enabled()) {
+          // VGG stem + relu + 2x2/s2 maxpool: [2 x wb] tiles, the epilogue writes only the pooled
+          // row (the 224x224x64 stem map never reaches HBM)
+          int wbp = 0;
+          for (int d = 64; d >= 2; d -= 2)
+            if (ow % d == 0) { wbp = d; break; }
+          if (wbp > 0) {
+            View o = b.compact(md.cout, oh / 2, ow / 2);
+            Op* op = nullptr;
+            if ((st = b.conv(cs, cur, o, relu, nullptr, &op)) != HAPI_OK) return st;
+            if (op->tc_mode == 4) {
+              op->pool2 = true;
+              op->conv_oh = oh; op->conv_ow = ow;
+              op->wb = wbp; op->hb = 2; op->nb = 1;
+              const ConvW& w = m->convs[op->conv];
+              op->flops = w.real_flops_per_px * (double)oh * ow;
+              op->bytes = ((double)cur.H * cur.W * cur.C + (double)o.H * o.W * o.C) * m->es;
+              op->desc += " +maxpool2/s2";
+              cur = o;
+              i = jp + 1;
+              break;
+            }
+            return set_error(HAPI_ERR_UNSUPPORTED, "VGG stem+pool: unexpected conv mode");
+          }
+        }
         View o = b.compact(md.cout, oh, ow);
         if ((st = b.conv(cs, cur, o, relu, nullptr)) != HAPI_OK) return st;
         cur = o;
@@ -1050,7 +1077,8 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
   const bool compact = cur.ld == cur.C && cur.coff == 0;
   const bool same_view = cur.buf >= 0 && last.out.buf == cur.buf && last.out.C == cur.C && last.out.ld == cur.ld &&
                          last.out.coff == cur.coff;
-  const bool can_direct = same_view && compact && last.t != OP_PACK_IN && !(last.t == OP_CONV && last.tc_mode == 8);
+  const bool can_direct = same_view && compact && last.t != OP_PACK_IN &&
+                          !(last.t == OP_CONV && (last.tc_mode == 8 || last.pool2));
   if (can_direct && last.t == OP_CONV) {
     last.out.buf = -1;
     last.nchw_out = true;
@@ -1195,6 +1223,9 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
     case OP_CONV: {
       const ConvW& w = m->convs[o.conv];
       ConvArgs a;
+      a.pool2 = o.pool2 ? 1 : 0;
+      a.ksplit = 1;
+      a.ws = nullptr;
       a.x = vptr(m, p, o.in, out);
       a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = w.cs; a.x_ld = o.in.ld;
       a.KH = w.kh; a.KW = w.kw; a.stride = w.stride; a.pad = w.pad;
@@ -1217,6 +1248,10 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.k2_diag = w.res_identity ? 1 : 0;
       if (o.s2d_view) {  // window view geometry (see finalize_tmaps)
         a.C = 64; a.KH = w.kh; a.KW = 1; a.stride = 1; a.pad = 0;
+      }
+      if (o.pool2) {  // the kernel iterates the conv map; y is the 2x2-pooled map
+        a.OH = o.conv_oh; a.OW = o.conv_ow;
+        a.M = (long long)nb * a.OH * a.OW;
       }
       if (o.tc_mode == 8) {  // the kernel iterates the stem map; y is the pooled map
         a.OH = o.conv_oh; a.OW = o.conv_ow;
@@ -1397,7 +1432,7 @@ hapi_status finalize_tmaps(hapi_model* m) {
         const bool win3 = w.kw == 8;
         void* base = static_cast<char*>(vptr(m, p, o.in, nullptr)) + (win3 ? 0 : o.in.ld * 2);
         const cuuint64_t px = (cuuint64_t)o.in.ld * 2;  // 32 B (s2d) / 16 B (win3)
-        const int stem_w = o.tc_mode == 8 ? o.conv_ow : o.out.W;
+        const int stem_w = (o.tc_mode == 8 || o.pool2) ? o.conv_ow : o.out.W;
         cuuint64_t dims[4] = {64, (cuuint64_t)stem_w, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
         cuuint64_t strides[3] = {px, px * o.in.W, px * o.in.W * o.in.H};
         cuuint32_t box[4] = {64, (cuuint32_t)o.wb, (cuuint32_t)o.hb, (cuuint32_t)o.nb};
