@@ -100,6 +100,47 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
     }
     return;
   }
+  if (layout == 4) {
+    // 3x3/s1/p1 stem on a 3-channel image (VGG), im2col in the pack: pixel (y, x) holds the
+    // 27 taps (r, s, c) of its 3x3 window (zeros outside the image) padded to 64 channels, so
+    // the stem is a 1x1 conv over plain NHWC rows.  One thread per pixel: 27 loads coalesced
+    // across the warp's consecutive pixels, 128 B of packed taps written as 8 x 16 B
+    const long long total = (long long)N * HW;
+    for (long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x; pix < total;
+         pix += (long long)gridDim.x * blockDim.x) {
+      const long long n = pix / HW;
+      const int rem = (int)(pix - n * HW), yy = rem / W, xx = rem - (rem / W) * W;
+      float v[28];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int iy = yy + r - 1;
+#pragma unroll
+        for (int s_ = 0; s_ < 3; ++s_) {
+          const int ix = xx + s_ - 1;
+          const bool in = iy >= 0 && iy < H && ix >= 0 && ix < W;
+          const float* src = img + n * 3 * HW + (long long)iy * W + ix;
+#pragma unroll
+          for (int c = 0; c < 3; ++c) v[(r * 3 + s_) * 3 + c] = in ? __ldg(src + c * HW) : 0.f;
+        }
+      }
+      v[27] = 0.f;
+      uint4* yo = reinterpret_cast<uint4*>(y) + pix * 8;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        uint4 o;
+        o.x = pack2(v[q * 8 + 0], v[q * 8 + 1]); o.y = pack2(v[q * 8 + 2], v[q * 8 + 3]);
+        o.z = pack2(v[q * 8 + 4], v[q * 8 + 5]); o.w = pack2(v[q * 8 + 6], v[q * 8 + 7]);
+        yo[q] = o;
+      }
+      uint4 o3;
+      o3.x = pack2(v[24], v[25]); o3.y = pack2(v[26], v[27]); o3.z = 0u; o3.w = 0u;
+      yo[3] = o3;
+      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int q = 4; q < 8; ++q) yo[q] = z;
+    }
+    return;
+  }
   if (layout == 3) {
     // 3x3/s1/p1 stem on a 3-channel image (VGG): NHWC padded to 8 channels with a zero border
     // (one row above and below, one column left, wp - W - 1 right), so the stem reads each
@@ -341,7 +382,8 @@ cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int
 
 cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, int wp, cudaStream_t st) {
   const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * wp
-                          : layout == 3 ? (long long)N * (H + 2) * wp : (long long)N * H * W;
+                          : layout == 3 ? (long long)N * (H + 2) * wp
+                          : (long long)N * H * W;
   launch_pdl(pack_input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, img, y, N, H, W, layout, wp);
   return cudaGetLastError();
 }

@@ -111,6 +111,14 @@ bool pair_enabled() {
   return on;
 }
 
+bool stem_col_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_STEM_COL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool win3_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_WIN3");
@@ -338,6 +346,8 @@ struct ConvSpec {
   int fh = 0, fw = 0;    // linear on a flattened (cin/(fh*fw), fh, fw) map: permute columns
   bool linear = false;
   bool s2d = false;      // 7x7/s2/p3 stem re-expressed as 4x4/s1/p2 on a 2x2 space-to-depth input
+  bool col3 = false;     // 3x3/s1/p1 stem on 3 channels (VGG) over the im2col-packed input: a 1x1
+                         // conv over 64 channels (k = (r*3+s)*3+c < 27)
   bool win3 = false;     // 3x3/s1/p1 stem on 3 channels (VGG) over the zero-bordered 8-channel input,
                          // each filter row one 8-pixel x 8-channel window: stored as KH=3, KW=8, C=8
   // fused downsample (bf16): out = conv(x1) + ds(x2) with ds a 1x1/stride2 conv + folded BN,
@@ -351,7 +361,7 @@ struct ConvSpec {
 
 hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   std::string key = s.wname + "|" + s.bname + "|" + s.fold_bn + "|" + s.pro_bn + "|" + std::to_string(s.cs) + "|" +
-                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "") + (s.win3 ? "|win3" : "") + "|" +
+                    std::to_string(s.fh) + "x" + std::to_string(s.fw) + (s.s2d ? "|s2d" : "") + (s.win3 ? "|win3" : "") + (s.col3 ? "|col3" : "") + "|" +
                     s.w2name + "|" +
                     s.fold2 + (s.res_identity ? "|resid" : "");
   auto it = m->conv_index.find(key);
@@ -383,8 +393,9 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
   cw.cout = s.cout;
   cw.kh = cw.kw = s.s2d ? 4 : kk;
   if (s.win3) cw.kw = 8;
+  if (s.col3) cw.kh = cw.kw = 1;
   cw.stride = s.s2d ? 1 : s.stride;
-  cw.pad = s.s2d ? 2 : (s.win3 ? 0 : s.pad);
+  cw.pad = s.s2d ? 2 : ((s.win3 || s.col3) ? 0 : s.pad);
   cw.K = cw.kh * cw.kw * s.cs;
   cw.real_flops_per_px = 2.0 * ((double)kk * kk * s.cin + s.cin2) * s.cout;
   cw.K2 = w2 ? s.cin2 : 0;
@@ -408,6 +419,14 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
       const int orr = 2 * r + aa - 1, ott = 2 * t + bb - 1;
       if (orr < 0 || orr >= kk || ott < 0 || ott >= kk) return 0.0;
       double v = w[(((int64_t)o * s.cin + ch) * kk + orr) * kk + ott];
+      if (!fs.empty()) v *= fs[o];
+      return v;
+    }
+    if (s.col3) {
+      // packed channel c = (r * 3 + t) * 3 + ch of the 1x1 conv
+      if (c >= 27) return 0.0;
+      const int rr = c / 9, tt = (c % 9) / 3, ch = c % 3;
+      double v = w[(((int64_t)o * s.cin + ch) * kk + rr) * kk + tt];
       if (!fs.empty()) v *= fs[o];
       return v;
     }
@@ -688,7 +707,8 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
                    m0.cin == 3 && H0 % 2 == 0 && W0 % 2 == 0;
   const bool win3 = start == 0 && m->bf16 && m0.kind == MK_CONV && m0.k == 3 && m0.stride == 1 && m0.pad == 1 &&
                     m0.cin == 3 && win3_enabled();
-  const int layout = !m->bf16 ? 0 : (s2d ? 2 : (win3 ? 3 : 1));
+  const bool col3 = win3 && stem_col_enabled();
+  const int layout = !m->bf16 ? 0 : (s2d ? 2 : (col3 ? 4 : (win3 ? 3 : 1)));
   View cur;
   if (start == 0) {
     // s2d padded width: 3 zero columns on the left, >= 1 on the right, and room for the
@@ -697,6 +717,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
     const int WP = std::max(sw, 2 * sS * spq) + 4;
     cur = layout == 2   ? b.compact(16, H0 / 2 + 3, WP)
           : layout == 3 ? b.compact(8, H0 + 2, W0 + 8)
+          : layout == 4 ? b.compact(64, H0, W0)
                         : b.compact(layout == 1 ? 8 : 3, H0, W0);
     Op o;
     o.t = OP_PACK_IN;
@@ -740,7 +761,8 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         cs.cin = md.cin; cs.cout = md.cout; cs.k = md.k; cs.stride = md.stride; cs.pad = md.pad;
         cs.cs = cur.C;
         cs.s2d = (i == 0 && s2d);
-        cs.win3 = (i == 0 && win3);
+        cs.col3 = (i == 0 && col3);
+        cs.win3 = (i == 0 && win3 && !col3);
         const int ih = (cs.s2d || cs.win3) ? H0 : cur.H, iw = (cs.s2d || cs.win3) ? W0 : cur.W;
         const int oh = out_dim(ih, md.k, md.stride, md.pad), ow = out_dim(iw, md.k, md.stride, md.pad);
         const int jp = j + (relu ? 1 : 0);
@@ -764,7 +786,7 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           i = jp + 1;
           break;
         }
-        if (cs.win3 && relu && jp < split && mods[jp].kind == MK_MAXPOOL && mods[jp].k == 2 && mods[jp].stride == 2 &&
+        if ((cs.win3 || cs.col3) && relu && jp < split && mods[jp].kind == MK_MAXPOOL && mods[jp].k == 2 && mods[jp].stride == 2 &&
             mods[jp].pad == 0 && oh % 2 == 0 && ow % 2 == 0 && stem_pool_enabled()) {
           // VGG stem + relu + 2x2/s2 maxpool: [2 x wb] tiles, the epilogue writes only the pooled
           // row (the 224x224x64 stem map never reaches HBM)
@@ -775,6 +797,13 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
             View o = b.compact(md.cout, oh / 2, ow / 2);
             Op* op = nullptr;
             if ((st = b.conv(cs, cur, o, relu, nullptr, &op)) != HAPI_OK) return st;
+            if (cs.col3 && op->tc_mode == 3) {
+              // the im2col-packed stem is a 1x1 conv: read it with mode-4 spatial boxes instead
+              // of flat 2D tiles so the epilogue sees [2 x wb] pixel blocks to pool
+              op->tc_mode = 4;
+              const size_t mp_ = op->desc.find("mode3");
+              if (mp_ != std::string::npos) op->desc.replace(mp_, 5, "mode4");
+            }
             if (op->tc_mode == 4) {
               op->pool2 = true;
               op->conv_oh = oh; op->conv_ow = ow;
