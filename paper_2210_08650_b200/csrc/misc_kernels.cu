@@ -103,41 +103,44 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
   if (layout == 4) {
     // 3x3/s1/p1 stem on a 3-channel image (VGG), im2col in the pack: pixel (y, x) holds the
     // 27 taps (r, s, c) of its 3x3 window (zeros outside the image) padded to 64 channels, so
-    // the stem is a 1x1 conv over plain NHWC rows.  One thread per pixel: 27 loads coalesced
-    // across the warp's consecutive pixels, 128 B of packed taps written as 8 x 16 B
+    // the stem is a 1x1 conv over plain NHWC rows.  One thread per pixel gathers its 27 taps
+    // (loads coalesced across the block's consecutive pixels) into shared memory; the block
+    // then writes its 256 x 128 B output span with consecutive 16-byte stores.
+    __shared__ uint4 tap_s[256][4];
     const long long total = (long long)N * HW;
-    for (long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x; pix < total;
-         pix += (long long)gridDim.x * blockDim.x) {
-      const long long n = pix / HW;
-      const int rem = (int)(pix - n * HW), yy = rem / W, xx = rem - (rem / W) * W;
-      float v[28];
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < total; base += (long long)gridDim.x * blockDim.x) {
+      const long long pix = base + threadIdx.x;
+      if (pix < total) {
+        const long long n = pix / HW;
+        const int rem = (int)(pix - n * HW), yy = rem / W, xx = rem - (rem / W) * W;
+        float v[28];
 #pragma unroll
-      for (int r = 0; r < 3; ++r) {
-        const int iy = yy + r - 1;
+        for (int r = 0; r < 3; ++r) {
+          const int iy = yy + r - 1;
 #pragma unroll
-        for (int s_ = 0; s_ < 3; ++s_) {
-          const int ix = xx + s_ - 1;
-          const bool in = iy >= 0 && iy < H && ix >= 0 && ix < W;
-          const float* src = img + n * 3 * HW + (long long)iy * W + ix;
+          for (int s_ = 0; s_ < 3; ++s_) {
+            const int ix = xx + s_ - 1;
+            const bool in = iy >= 0 && iy < H && ix >= 0 && ix < W;
+            const float* src = img + n * 3 * HW + (long long)iy * W + ix;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) v[(r * 3 + s_) * 3 + c] = in ? __ldg(src + c * HW) : 0.f;
+            for (int c = 0; c < 3; ++c) v[(r * 3 + s_) * 3 + c] = in ? __ldg(src + c * HW) : 0.f;
+          }
         }
-      }
-      v[27] = 0.f;
-      uint4* yo = reinterpret_cast<uint4*>(y) + pix * 8;
+        v[27] = 0.f;
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        uint4 o;
-        o.x = pack2(v[q * 8 + 0], v[q * 8 + 1]); o.y = pack2(v[q * 8 + 2], v[q * 8 + 3]);
-        o.z = pack2(v[q * 8 + 4], v[q * 8 + 5]); o.w = pack2(v[q * 8 + 6], v[q * 8 + 7]);
-        yo[q] = o;
+        for (int q = 0; q < 3; ++q)
+          tap_s[threadIdx.x][q] = make_uint4(pack2(v[q * 8 + 0], v[q * 8 + 1]), pack2(v[q * 8 + 2], v[q * 8 + 3]),
+                                             pack2(v[q * 8 + 4], v[q * 8 + 5]), pack2(v[q * 8 + 6], v[q * 8 + 7]));
+        tap_s[threadIdx.x][3] = make_uint4(pack2(v[24], v[25]), pack2(v[26], v[27]), 0u, 0u);
       }
-      uint4 o3;
-      o3.x = pack2(v[24], v[25]); o3.y = pack2(v[26], v[27]); o3.z = 0u; o3.w = 0u;
-      yo[3] = o3;
-      const uint4 z = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-      for (int q = 4; q < 8; ++q) yo[q] = z;
+      __syncthreads();
+      const long long npix = total - base < (long long)blockDim.x ? total - base : (long long)blockDim.x;
+      uint4* yo = reinterpret_cast<uint4*>(y) + base * 8;
+      for (int t = threadIdx.x; t < npix * 8; t += blockDim.x) {
+        const int p = t >> 3, part = t & 7;
+        yo[t] = part < 4 ? tap_s[p][part] : make_uint4(0u, 0u, 0u, 0u);
+      }
+      __syncthreads();
     }
     return;
   }
