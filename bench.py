@@ -72,6 +72,14 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:  # noqa: BLE001
             self.proc = None
+        # nvidia-smi takes ~0.1-0.3 s to start: wait for its first sample so that a short timed
+        # region (DenseNet s=9: ~35 ms) is still covered by the 20 ms sampling that follows.
+        self.first = []
+        if self.proc:
+            import threading
+            t = threading.Thread(target=lambda: self.first.append(self.proc.stdout.readline()), daemon=True)
+            t.start()
+            t.join(5.0)
         return self
 
     def __exit__(self, *a):
@@ -84,6 +92,8 @@ class ClockSampler:
                 self.proc.kill()
                 out = ""
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            if not self.lines:  # region shorter than one sampling period: keep the pre-region sample
+                self.lines = [ln for ln in self.first if ln and ln.strip()]
 
     def summary(self):
         sm, mx, reasons, pw = [], None, set(), []
