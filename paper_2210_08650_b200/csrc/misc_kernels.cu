@@ -226,6 +226,43 @@ __global__ void pool_kernel(const PoolArgs a) {
   }
 }
 
+// 2x2/s2/p0 pooling on bf16 NHWC (VGG maxpools, DenseNet transition avgpools): every window is
+// in bounds, so one thread reads its four 16-byte channel vectors with no bounds tests and 32-bit
+// index arithmetic.  Same operations in the same order as pool_kernel (bitwise identical).
+template <int MODE>
+__global__ void __launch_bounds__(256) pool2x2_bf16_kernel(const PoolArgs a) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const unsigned cg = (unsigned)a.C / 8u;
+  const unsigned total = (unsigned)a.N * a.OH * a.OW * cg;
+  const __nv_bfloat16* x = static_cast<const __nv_bfloat16*>(a.x);
+  __nv_bfloat16* y = static_cast<__nv_bfloat16*>(a.y);
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const unsigned pix = i / cg;
+    const unsigned c = (i - pix * cg) * 8u;
+    const unsigned row = pix / (unsigned)a.OW;  // n * OH + oh
+    const unsigned ow = pix - row * (unsigned)a.OW;
+    const unsigned n = row / (unsigned)a.OH;
+    const unsigned oh = row - n * (unsigned)a.OH;
+    const __nv_bfloat16* p0 = x + ((size_t)(n * a.H + 2u * oh) * a.W + 2u * ow) * a.x_ld + c;
+    const __nv_bfloat16* p1 = p0 + (size_t)a.W * a.x_ld;
+    float f[4][8];
+    load_vec<__nv_bfloat16, 8>(p0, f[0]);
+    load_vec<__nv_bfloat16, 8>(p0 + a.x_ld, f[1]);
+    load_vec<__nv_bfloat16, 8>(p1, f[2]);
+    load_vec<__nv_bfloat16, 8>(p1 + a.x_ld, f[3]);
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = MODE == 0 ? -INFINITY : 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v = MODE == 0 ? fmaxf(v, f[t][j]) : v + f[t][j];
+      acc[j] = MODE == 0 ? v : v * 0.25f;
+    }
+    store_vec<__nv_bfloat16, 8>(y + (size_t)pix * a.y_ld + c, acc);
+  }
+}
+
 template <typename T, int V>
 __global__ void adaptive_kernel(const AdaptiveArgs a) {
   griddep_launch_dependents();
@@ -246,13 +283,25 @@ __global__ void adaptive_kernel(const AdaptiveArgs a) {
     float acc[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[j] = 0.f;
-    for (int ih = h0; ih < h1; ++ih)
-      for (int iw = w0; iw < w1; ++iw) {
-        float f[V];
-        load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f);
+    // The bin's pixels in row-major order, loaded in groups of 8 independent loads and then
+    // accumulated in that same order (a serial load-add chain is latency-bound: ResNet's 7x7
+    // global pool would wait 49 times on HBM).
+    const int bw = w1 - w0, cnt = (h1 - h0) * bw;
+    for (int q0 = 0; q0 < cnt; q0 += 8) {
+      float f[8][V];
 #pragma unroll
-        for (int j = 0; j < V; ++j) acc[j] += a.relu_in ? fmaxf(f[j], 0.f) : f[j];
-      }
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < cnt) {
+          const int ih = h0 + (q0 + u) / bw, iw = w0 + (q0 + u) % bw;
+          load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f[u]);
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < cnt) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[j] += a.relu_in ? fmaxf(f[u][j], 0.f) : f[u][j];
+        }
+    }
     const float inv = 1.f / (float)((h1 - h0) * (w1 - w0));
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[j] *= inv;
@@ -391,10 +440,26 @@ cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, in
   return cudaGetLastError();
 }
 
+// HAPI_POOL_GENERIC=1: every pool through pool_kernel (A/B of the 2x2 specialisation).
+static bool pool_generic() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_POOL_GENERIC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 cudaError_t pool_launch(const PoolArgs& a, int is_bf16, cudaStream_t st) {
   const long long pix = (long long)a.N * a.OH * a.OW;
   if (is_bf16) {
-    if (a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y))
+    const bool vec8 = a.C % 8 == 0 && a.x_ld % 8 == 0 && a.y_ld % 8 == 0 && aligned16(a.x) && aligned16(a.y);
+    if (vec8 && a.k == 2 && a.stride == 2 && a.pad == 0 && a.OH * 2 <= a.H && a.OW * 2 <= a.W &&
+        pix * (a.C / 8) < (1ll << 31) && !pool_generic()) {
+      if (a.mode == 0)
+        launch_pdl(pool2x2_bf16_kernel<0>, dim3(grid_for(pix * (a.C / 8), 256)), dim3(256), 0, st, a);
+      else
+        launch_pdl(pool2x2_bf16_kernel<1>, dim3(grid_for(pix * (a.C / 8), 256)), dim3(256), 0, st, a);
+    } else if (vec8)
       launch_pdl(pool_kernel<__nv_bfloat16, 8>, dim3(grid_for(pix * (a.C / 8), 256)), dim3(256), 0, st, a);
     else
       launch_pdl(pool_kernel<__nv_bfloat16, 1>, dim3(grid_for(pix * a.C, 256)), dim3(256), 0, st, a);

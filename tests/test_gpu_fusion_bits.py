@@ -53,6 +53,8 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("resnet50", 21, 100, 3, "HAPI_SUB_STORE", None, "0"),  # ... odd 25x25 map (13x13 subsample)
     ("vgg11", 3, 72, 3, "HAPI_STEM_POOL", None, "0"),       # VGG stem + 2x2 maxpool in the epilogue
     ("vgg11", 11, 96, 2, "HAPI_STEM_POOL", None, "0"),
+    ("vgg11", 21, 100, 2, "HAPI_POOL_GENERIC", None, "1"),      # 2x2/s2 pool kernel; odd 25x25 map
+    ("densenet121", 20, 64, 3, "HAPI_POOL_GENERIC", None, "1"),  # ... transition avgpools
 ])
 def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off):
     fused = _run(tmp_path, {flag: on} if on else {}, arch, split, size, n, "on")
