@@ -283,25 +283,13 @@ __global__ void adaptive_kernel(const AdaptiveArgs a) {
     float acc[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[j] = 0.f;
-    // The bin's pixels in row-major order, loaded in groups of 8 independent loads and then
-    // accumulated in that same order (a serial load-add chain is latency-bound: ResNet's 7x7
-    // global pool would wait 49 times on HBM).
-    const int bw = w1 - w0, cnt = (h1 - h0) * bw;
-    for (int q0 = 0; q0 < cnt; q0 += 8) {
-      float f[8][V];
+    for (int ih = h0; ih < h1; ++ih)
+      for (int iw = w0; iw < w1; ++iw) {
+        float f[V];
+        load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f);
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q0 + u < cnt) {
-          const int ih = h0 + (q0 + u) / bw, iw = w0 + (q0 + u) % bw;
-          load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f[u]);
-        }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q0 + u < cnt) {
-#pragma unroll
-          for (int j = 0; j < V; ++j) acc[j] += a.relu_in ? fmaxf(f[u][j], 0.f) : f[u][j];
-        }
-    }
+        for (int j = 0; j < V; ++j) acc[j] += a.relu_in ? fmaxf(f[j], 0.f) : f[j];
+      }
     const float inv = 1.f / (float)((h1 - h0) * (w1 - w0));
 #pragma unroll
     for (int j = 0; j < V; ++j) acc[j] *= inv;
@@ -384,7 +372,10 @@ __global__ void __launch_bounds__(256) pack_output_v8_kernel(const __nv_bfloat16
                                                              int x_ld, __nv_bfloat16* __restrict__ y) {
   griddep_launch_dependents();
   griddep_wait();
-  __shared__ __align__(16) __nv_bfloat16 tile[64][64 + 8];  // [channel][pixel], padded rows
+  // [channel][pixel]; the 16-byte pixel chunk of row r is stored at chunk ^ (r >> 3) so the
+  // transposing scalar stores of a warp (8 channel rows 8 apart) hit 8 different bank groups
+  // (a padded 72-element row maps rows 8 apart to the same bank: 8-way conflicts, 3.2 TB/s).
+  __shared__ __align__(16) __nv_bfloat16 tile[64][64];
   const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
   const long long n = blockIdx.z;
   const int t = threadIdx.x;
@@ -397,7 +388,7 @@ __global__ void __launch_bounds__(256) pack_output_v8_kernel(const __nv_bfloat16
     if (p < HW && c < C) v = __ldg(reinterpret_cast<const uint4*>(x + (n * HW + p) * x_ld + c));
     const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) tile[cc + j][pp] = e[j];
+    for (int j = 0; j < 8; ++j) tile[cc + j][(((pp >> 3) ^ ((cc + j) >> 3)) << 3) | (pp & 7)] = e[j];
   }
   __syncthreads();
 #pragma unroll
@@ -406,7 +397,8 @@ __global__ void __launch_bounds__(256) pack_output_v8_kernel(const __nv_bfloat16
     const int cc = idx >> 3, pp = (idx & 7) * 8;
     const int c = c0 + cc, p = p0 + pp;
     if (c < C && p < HW)
-      *reinterpret_cast<uint4*>(y + (n * C + c) * HW + p) = *reinterpret_cast<const uint4*>(&tile[cc][pp]);
+      *reinterpret_cast<uint4*>(y + (n * C + c) * HW + p) =
+          *reinterpret_cast<const uint4*>(&tile[cc][((pp >> 3) ^ (cc >> 3)) << 3]);
   }
 }
 
