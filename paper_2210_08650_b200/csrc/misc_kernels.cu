@@ -496,6 +496,31 @@ cudaError_t bn_act_launch(const EltArgs& a, int is_bf16, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Small maps whose HW is not a multiple of 8 (7x7 splits: VGG s=21, ResNet s=20): one block per
+// (image, 64-channel group).  The group's output is one contiguous span of 64 * HW elements, so
+// the block gathers its HW x 64 input with 16-byte loads, transposes into a shared copy of that
+// span, and writes it back with 16-byte stores.
+__global__ void __launch_bounds__(256) pack_output_span_kernel(const __nv_bfloat16* __restrict__ x, int HW, int C,
+                                                               int x_ld, __nv_bfloat16* __restrict__ y) {
+  griddep_launch_dependents();
+  griddep_wait();
+  extern __shared__ __align__(16) unsigned char span_raw[];
+  __nv_bfloat16* span = reinterpret_cast<__nv_bfloat16*>(span_raw);  // [64][HW]
+  const int c0 = blockIdx.x * 64;
+  const long long n = blockIdx.y;
+  for (int idx = threadIdx.x; idx < HW * 8; idx += blockDim.x) {
+    const int p = idx >> 3, cc = (idx & 7) * 8;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(x + (n * HW + p) * x_ld + c0 + cc));
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) span[(cc + j) * HW + p] = e[j];
+  }
+  __syncthreads();
+  uint4* dst = reinterpret_cast<uint4*>(y + (n * C + c0) * HW);
+  const uint4* src = reinterpret_cast<const uint4*>(span);
+  for (int i = threadIdx.x; i < HW * 8; i += blockDim.x) dst[i] = src[i];  // 64 * HW / 8 vectors
+}
+
 cudaError_t pack_output_launch(const void* x, int N, int HW, int C, int x_ld, void* y, int is_bf16, cudaStream_t st) {
   const size_t es = is_bf16 ? 2 : 4;
   if (HW == 1) {  // NHWC == NCHW: a strided row copy
@@ -503,6 +528,11 @@ cudaError_t pack_output_launch(const void* x, int N, int HW, int C, int x_ld, vo
   }
   if (is_bf16 && HW % 8 == 0 && C % 8 == 0 && x_ld % 8 == 0 && aligned16(x) && aligned16(y)) {
     launch_pdl(pack_output_v8_kernel, dim3((HW + 63) / 64, (C + 63) / 64, N), dim3(256), 0, st,
+               static_cast<const __nv_bfloat16*>(x), HW, C, x_ld, static_cast<__nv_bfloat16*>(y));
+    return cudaGetLastError();
+  }
+  if (is_bf16 && C % 64 == 0 && HW <= 256 && x_ld % 8 == 0 && aligned16(x) && aligned16(y) && N <= 65535) {
+    launch_pdl(pack_output_span_kernel, dim3(C / 64, N), dim3(256), (size_t)64 * HW * 2, st,
                static_cast<const __nv_bfloat16*>(x), HW, C, x_ld, static_cast<__nv_bfloat16*>(y));
     return cudaGetLastError();
   }

@@ -1108,7 +1108,11 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
                          last.out.coff == cur.coff;
   const bool can_direct = same_view && compact && last.t != OP_PACK_IN &&
                           !(last.t == OP_CONV && (last.tc_mode == 8 || last.pool2));
-  if (can_direct && last.t == OP_CONV) {
+  static const bool nchw_epi = [] {  // HAPI_NCHW_EPI=0: last conv stores NHWC, then the split pack
+    const char* e = std::getenv("HAPI_NCHW_EPI");
+    return !(e && e[0] == '0');
+  }();
+  if (can_direct && last.t == OP_CONV && nchw_epi) {
     last.out.buf = -1;
     last.nchw_out = true;
   } else if (can_direct && cur.H == 1 && cur.W == 1 && (last.t == OP_POOL || last.t == OP_ADAPTIVE || last.t == OP_BNACT)) {
