@@ -55,6 +55,9 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("vgg11", 11, 96, 2, "HAPI_STEM_POOL", None, "0"),
     ("vgg11", 21, 100, 2, "HAPI_POOL_GENERIC", None, "1"),      # 2x2/s2 pool kernel; odd 25x25 map
     ("densenet121", 20, 64, 3, "HAPI_POOL_GENERIC", None, "1"),  # ... transition avgpools
+    ("resnet50", 20, 224, 2, "HAPI_NCHW_EPI", None, "0"),   # NCHW epilogue vs NHWC + span pack (7x7)
+    ("resnet50", 21, 96, 6, "HAPI_NCHW_EPI", None, "0"),    # ... 3x3 split map
+    ("resnet18", 10, 200, 3, "HAPI_NCHW_EPI", None, "0"),   # ... 7x7, 512 channels
 ])
 def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off):
     fused = _run(tmp_path, {flag: on} if on else {}, arch, split, size, n, "on")
