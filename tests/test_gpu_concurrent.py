@@ -3,7 +3,7 @@ assigns each queued request a COS batch under one HBM budget, each request runs 
 model on its own stream concurrently, and
 
 * every request's split output is bitwise identical to running it alone (requests share no
-  state: separate arenas, weights and streams);
+  state: separate arenas, weights and streams), and matches the oracle on sampled images;
 * the device memory the models own together stays within the budget the adaptation was given
   (Eq. 4's constraint, with est = W + b*P over-estimating each model, section 4.3).
 """
@@ -12,6 +12,8 @@ import pytest
 
 import hapi_inputs
 from oracle import planner
+from tests.gpu_helpers import oracle_all
+from tests.parity_check import check_close
 
 pytestmark = pytest.mark.gpu
 
@@ -58,5 +60,10 @@ def test_concurrent_requests_match_sequential_and_fit_budget():
     torch.cuda.synchronize()
     for a, out in zip(alone, outs):
         assert torch.equal(a.view(torch.int16), out.view(torch.int16))
+    for (arch, s, n), out in zip(queue, outs):
+        sel = [0, n - 1]
+        ref = oracle_all(arch, 21, 22 + s, n, upto=s, sel=sel)[s - 1]
+        got = out.float().cpu().numpy().reshape(n, -1)[sel]
+        check_close(got, ref, "bf16", f"concurrent {arch} s={s}")
     for m in models:
         m.close()

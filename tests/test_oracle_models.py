@@ -99,3 +99,41 @@ def test_batch_invariance_oracle():
     full = prefix.prefix_forward("resnet18", P, x, 10)
     one = prefix.prefix_forward("resnet18", P, x[1:2], 10)
     np.testing.assert_allclose(full[1:2], one, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("act", ["f32", "bf16"])
+@pytest.mark.parametrize("arch", list(TV))
+def test_estimate_matches_torchvision_brute_force(arch, act):
+    """planner.estimate(arch, s, b) = W(s) + b * P(s) (section 4.3), pinned
+    against a construction that shares nothing with oracle/archs.py or oracle/planner.py:
+    W(s) sums torchvision's own parameters of the first s layers of tv_layers (weights of
+    rank >= 2 at the activation width, biases / BN affine at 4 bytes; running buffers are
+    buffers, not parameters), P(s) = max over i <= s of input + output bytes of layer i
+    measured by running the torchvision modules on one 224x224 image (Alg. 1 lines 1-5's
+    profiling run), l_0 = the fp32 input.  Every s and three batches, and the split
+    planner's est_bytes for the batch it picks equals the same value (an index slip such as
+    W(s+1) or P(s-1) fails here)."""
+    from oracle import planner
+    ab = 2 if act == "bf16" else 4
+    model = TV[arch](weights=None).float().eval()
+    layers = tv_layers(arch, model)
+    names = [n for n, _ in layers]
+    owner = {}
+    for pname, prm in model.named_parameters():
+        mod = max((n for n in names if pname.startswith(n + ".")), key=len)
+        owner.setdefault(mod, []).append(prm)
+    t = torch.zeros(1, 3, 224, 224)
+    sizes = [3 * 224 * 224 * 4]
+    with torch.no_grad():
+        for _, fn in layers:
+            t = fn(t)
+            sizes.append(t.numel() * ab)
+    W = P = 0
+    for s, n in enumerate(names, start=1):
+        W += sum(p.numel() * (ab if p.dim() >= 2 else 4) for p in owner.get(n, []))
+        P = max(P, sizes[s - 1] + sizes[s])
+        for b in (1, 25, 512):
+            assert planner.estimate(arch, s, b, act) == W + b * P, (arch, s, b)
+        budget = W + 77 * P + 5
+        r = planner.choose_split(planner.SplitQuery(arch, s, 1, 1, budget, b_min=1, b_max=100, act=act))
+        assert r.split_idx == s and r.cos_batch == 77 and r.est_bytes == W + 77 * P
