@@ -169,7 +169,14 @@ typedef struct {
                                     kept on the device */
   uint32_t max_batch;        /* arena sized for this many images per launch (normally the
                                  cos_batch of hapi_choose_split); larger calls are chunked */
-  int device;                /* CUDA ordinal */
+  int device;                /* CUDA ordinal.  Every call on the model switches to it and
+                                 restores the caller's current device on return. */
+  uint32_t host_chunk;       /* images per chunk of hapi_prefix_forward_host (0: no host
+                                path).  Its staging -- 2 x host_chunk images in and split
+                                outputs out, the double-buffered DRAM<->GPU transfers of
+                                Eq. 1's C11 * B * (l0 + l_split) terms, PAPER.md:204-206 --
+                                is allocated here at create time and counted in
+                                hapi_model_device_bytes; min(host_chunk, max_batch) is used */
 } hapi_model_desc;
 
 /* Builds a model: reads the fp32 host params (read during the call only; caller keeps
@@ -188,7 +195,9 @@ HAPI_API hapi_status hapi_model_set_stream(hapi_model *m, void *cuda_stream);
  * layer-split_idx activations as contiguous NCHW [batch,C,H,W] (or [batch,F] inside a
  * classifier) in the model's act dtype (reading R11).  Images are processed in chunks
  * of max_batch in order; results do not depend on chunking (a8).  Asynchronous on the
- * model's stream; never allocates.  images/out must not alias each other or the model.
+ * model's stream; never allocates device memory (the first call per (split, chunk size)
+ * captures and instantiates a CUDA graph; later calls with other buffers update it in
+ * place).  images/out must not alias each other or the model.
  * Errors: INVALID_ARGUMENT (batch 0, split outside [min_split,max_split], null),
  * CUDA (launch failure or an earlier asynchronous fault). */
 HAPI_API hapi_status hapi_prefix_forward(hapi_model *m, uint32_t split_idx, const float *images,
@@ -214,12 +223,17 @@ HAPI_API hapi_status hapi_suffix_forward(hapi_model *m, uint32_t end_idx, const 
 
 /* End-to-end variant with HOST buffers (pinned or pageable): images [batch,3,H,W] fp32
  * host -> device copies, prefix forward, device -> host copy of the split output into
- * host `out`, pipelined in max_batch chunks over two streams (H2D of chunk i+1 overlaps
- * compute of chunk i).  Synchronous: returns when `out` is filled. */
+ * host `out`, pipelined in chunks of at most desc.host_chunk images (a half-size first
+ * chunk: its H2D is the pipeline fill) over two copy streams (H2D of chunk i+1 and D2H of
+ * chunk i-1 overlap compute of chunk i; "moving data to and from GPU").
+ * Uses only the staging allocated at create time (never allocates).  Synchronous:
+ * returns when `out` is filled.  Errors: INVALID_ARGUMENT (host_chunk was 0, batch 0,
+ * split out of range, null), CUDA. */
 HAPI_API hapi_status hapi_prefix_forward_host(hapi_model *m, uint32_t split_idx, const float *images,
                                      uint64_t batch, void *out);
 
-/* Device bytes owned by the model: packed weights (+bias/BN vectors) and the arena. */
+/* Device bytes owned by the model: packed weights (+bias/BN vectors), and the activation
+ * arena plus the host-path staging (desc.host_chunk) in *arena_bytes. */
 HAPI_API hapi_status hapi_model_device_bytes(const hapi_model *m, uint64_t *weight_bytes, uint64_t *arena_bytes);
 
 /* Per-launch profile of split_idx's plan (for bench.py's roofline): number of kernel

@@ -1,4 +1,4 @@
-"""Oracle operators: the textbook eval-mode definitions, NCHW, float64.
+"""Oracle operators: the textbook eval-mode definitions, NCHW, float64 (FLOAT).
 
 TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
 ``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this package.
@@ -17,6 +17,26 @@ import numpy as np
 
 BN_EPS = 1e-5
 
+# Working precision of every operator: float64 for parity (the oracle proper).  bench.py's
+# cpu_baseline leg alone switches to float32 ("the same code in fp32 mode").
+FLOAT = np.float64
+
+
+class precision:
+    """with ops.precision(np.float32): ... -- run the same definitions at another width."""
+
+    def __init__(self, dt):
+        self.dt = dt
+
+    def __enter__(self):
+        global FLOAT
+        self.prev, FLOAT = FLOAT, self.dt
+        return self
+
+    def __exit__(self, *a):
+        global FLOAT
+        FLOAT = self.prev
+
 
 def out_size(h: int, k: int, stride: int, pad: int) -> int:
     """H_out = floor((H + 2p - k) / s) + 1 (no dilation, ceil_mode=False)."""
@@ -28,35 +48,35 @@ def conv2d(x: np.ndarray, w: np.ndarray, b, stride: int, pad: int) -> np.ndarray
 
     Explicit im2col (every (r,t) tap gathered into its own column block) followed by
     one matmul per image over K = C*R*S."""
-    x = np.asarray(x, dtype=np.float64)
-    w = np.asarray(w, dtype=np.float64)
+    x = np.asarray(x, dtype=FLOAT)
+    w = np.asarray(w, dtype=FLOAT)
     n, c, h, wd = x.shape
     o, c2, r, s = w.shape
     assert c == c2, (x.shape, w.shape)
     oh, ow = out_size(h, r, stride, pad), out_size(wd, s, stride, pad)
     xp = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
     wm = w.reshape(o, c * r * s)
-    out = np.empty((n, o, oh, ow), dtype=np.float64)
+    out = np.empty((n, o, oh, ow), dtype=FLOAT)
     for i in range(n):  # one image at a time bounds the im2col buffer
-        cols = np.empty((c, r, s, oh, ow), dtype=np.float64)
+        cols = np.empty((c, r, s, oh, ow), dtype=FLOAT)
         for dr in range(r):
             for ds in range(s):
                 cols[:, dr, ds] = xp[i, :, dr: dr + stride * (oh - 1) + 1: stride,
                                      ds: ds + stride * (ow - 1) + 1: stride]
         out[i] = (wm @ cols.reshape(c * r * s, oh * ow)).reshape(o, oh, ow)
     if b is not None:
-        out += np.asarray(b, dtype=np.float64)[None, :, None, None]
+        out += np.asarray(b, dtype=FLOAT)[None, :, None, None]
     return out
 
 
 def batchnorm_eval(x, gamma, beta, mean, var, eps: float = BN_EPS):
     """gamma * (x - mean) / sqrt(var + eps) + beta, per channel (axis 1)."""
     sh = (1, -1) + (1,) * (x.ndim - 2)
-    g = np.asarray(gamma, np.float64).reshape(sh)
-    b = np.asarray(beta, np.float64).reshape(sh)
-    m = np.asarray(mean, np.float64).reshape(sh)
-    v = np.asarray(var, np.float64).reshape(sh)
-    return g * (np.asarray(x, np.float64) - m) / np.sqrt(v + eps) + b
+    g = np.asarray(gamma, FLOAT).reshape(sh)
+    b = np.asarray(beta, FLOAT).reshape(sh)
+    m = np.asarray(mean, FLOAT).reshape(sh)
+    v = np.asarray(var, FLOAT).reshape(sh)
+    return g * (np.asarray(x, FLOAT) - m) / np.sqrt(v + eps) + b
 
 
 def relu(x):
@@ -67,9 +87,9 @@ def maxpool2d(x, k: int, stride: int, pad: int):
     """max over the k x k window; padding = -inf; ceil_mode=False."""
     n, c, h, w = x.shape
     oh, ow = out_size(h, k, stride, pad), out_size(w, k, stride, pad)
-    xp = np.pad(np.asarray(x, np.float64), ((0, 0), (0, 0), (pad, pad), (pad, pad)),
+    xp = np.pad(np.asarray(x, FLOAT), ((0, 0), (0, 0), (pad, pad), (pad, pad)),
                 constant_values=-np.inf)
-    out = np.full((n, c, oh, ow), -np.inf)
+    out = np.full((n, c, oh, ow), -np.inf, dtype=FLOAT)
     for dr in range(k):
         for ds in range(k):
             out = np.maximum(out, xp[:, :, dr: dr + stride * (oh - 1) + 1: stride,
@@ -81,10 +101,10 @@ def avgpool2d(x, k: int, stride: int):
     """mean over the k x k window, no padding (DenseNet transition: k = s = 2)."""
     n, c, h, w = x.shape
     oh, ow = out_size(h, k, stride, 0), out_size(w, k, stride, 0)
-    acc = np.zeros((n, c, oh, ow))
+    acc = np.zeros((n, c, oh, ow), dtype=FLOAT)
     for dr in range(k):
         for ds in range(k):
-            acc += np.asarray(x, np.float64)[:, :, dr: dr + stride * (oh - 1) + 1: stride,
+            acc += np.asarray(x, FLOAT)[:, :, dr: dr + stride * (oh - 1) + 1: stride,
                                              ds: ds + stride * (ow - 1) + 1: stride]
     return acc / (k * k)
 
@@ -96,17 +116,17 @@ def adaptive_bins(insz: int, outsz: int):
 
 def adaptive_avgpool2d(x, oh: int, ow: int):
     n, c, h, w = x.shape
-    out = np.empty((n, c, oh, ow))
+    out = np.empty((n, c, oh, ow), dtype=FLOAT)
     for i, (h0, h1) in enumerate(adaptive_bins(h, oh)):
         for j, (w0, w1) in enumerate(adaptive_bins(w, ow)):
-            out[:, :, i, j] = np.asarray(x, np.float64)[:, :, h0:h1, w0:w1].mean(axis=(2, 3))
+            out[:, :, i, j] = np.asarray(x, FLOAT)[:, :, h0:h1, w0:w1].mean(axis=(2, 3))
     return out
 
 
 def flatten(x):
-    return np.asarray(x, np.float64).reshape(x.shape[0], -1)
+    return np.asarray(x, FLOAT).reshape(x.shape[0], -1)
 
 
 def linear(x, w, b):
     """x W^T + b on the flattened input."""
-    return flatten(x) @ np.asarray(w, np.float64).T + np.asarray(b, np.float64)[None, :]
+    return flatten(x) @ np.asarray(w, FLOAT).T + np.asarray(b, FLOAT)[None, :]

@@ -14,14 +14,14 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import archs
+from . import archs, ops
 
 
 def prefix_forward(arch: str, params, images: np.ndarray, split_idx: int) -> np.ndarray:
     mods = archs.layers(arch)
     if not 1 <= split_idx <= len(mods):
         raise ValueError(f"split_idx {split_idx} not in [1, {len(mods)}]")
-    x = np.asarray(images, dtype=np.float64)
+    x = np.asarray(images, dtype=ops.FLOAT)
     for m in mods[:split_idx]:
         x = m.fwd(x, params)
     return x
@@ -31,7 +31,7 @@ def prefix_forward_all(arch: str, params, images: np.ndarray, upto: int | None =
     """Outputs of every layer 1..upto (one pass; used by the profiling-run pin)."""
     mods = archs.layers(arch)
     upto = len(mods) if upto is None else upto
-    x = np.asarray(images, dtype=np.float64)
+    x = np.asarray(images, dtype=ops.FLOAT)
     outs = []
     for m in mods[:upto]:
         x = m.fwd(x, params)
@@ -44,7 +44,7 @@ def suffix_forward(arch: str, params, acts: np.ndarray, start_idx: int, end_idx:
     frozen suffix, PAPER.md:734 / SURVEY 8(f) f3): the same per-layer definitions, begun
     later.  acts: [B, C, H, W] (or [B, F]) as layer start_idx produces it."""
     mods = archs.layers(arch)
-    x = np.asarray(acts, dtype=np.float64)
+    x = np.asarray(acts, dtype=ops.FLOAT)
     for m in mods[start_idx:end_idx]:
         x = m.fwd(x, params)
     return x

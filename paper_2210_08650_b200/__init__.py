@@ -109,14 +109,21 @@ def hapi_param_table(arch):
     return out
 
 
+def _need(cond: bool, msg: str):
+    if not cond:
+        raise ValueError(msg)
+
+
 class Model:
     """hapi_model handle.  `params`: sequence of fp32 C-contiguous arrays (numpy or CPU
     torch tensors) in hapi_param_table order."""
 
     def __init__(self, arch, act, params: Sequence, max_batch: int, min_split: int, max_split: Optional[int] = None,
-                 in_h: int = 224, in_w: int = 224, device: int = 0, start_idx: int = 0):
+                 in_h: int = 224, in_w: int = 224, device: int = 0, start_idx: int = 0, host_chunk: int = 0):
         """start_idx > 0: a client-side suffix model (input = layer start_idx's NCHW output,
-        computes layers start_idx+1 .. split; use forward_suffix)."""
+        computes layers start_idx+1 .. split; use forward_suffix).  host_chunk > 0: staging
+        for forward_host (chunks of that many images) is allocated here; -1 picks the
+        measured default (3/16 of max_batch rounded to 16, at least 64, at most max_batch)."""
         import numpy as np
         max_split = min_split if max_split is None else max_split
         self.arch, self.act = arch, act
@@ -124,7 +131,9 @@ class Model:
         self.min_split, self.max_split = min_split, max_split
         keep = [np.ascontiguousarray(np.asarray(p, dtype=np.float32)) for p in params]
         ptrs = (C.c_void_p * len(keep))(*[p.ctypes.data for p in keep])
-        d = _lib.ModelDesc(_arch(arch), _dt(act), in_h, in_w, min_split, max_split, max_batch, device)
+        if host_chunk < 0:
+            host_chunk = max_batch if max_batch < 256 else min(max_batch, max(64, (max_batch * 3 // 16 + 15) // 16 * 16))
+        d = _lib.ModelDesc(_arch(arch), _dt(act), in_h, in_w, min_split, max_split, max_batch, device, host_chunk)
         h = C.c_void_p()
         if start_idx:
             _check(_lib.hapi_model_create_suffix(C.byref(d), start_idx, ptrs, len(keep), C.byref(h)))
@@ -149,10 +158,41 @@ class Model:
     def out_shape(self, split_idx: int, batch: int):
         return batch, self.out_bytes[split_idx - 1] // (4 if self.act == "f32" else 2)
 
+    def _split_bytes(self, idx: int) -> int:
+        _need(1 <= idx <= len(self.out_bytes), f"layer index {idx} outside [1, {len(self.out_bytes)}]")
+        return self.out_bytes[idx - 1]
+
+    def _check_images(self, images, on_device: bool):
+        import torch
+        _need(isinstance(images, torch.Tensor), "images must be a torch tensor")
+        _need(images.dtype == torch.float32, f"images must be float32, got {images.dtype}")
+        _need(images.dim() == 4 and tuple(images.shape[1:]) == (3, self.in_h, self.in_w),
+              f"images must be [N,3,{self.in_h},{self.in_w}], got {tuple(images.shape)}")
+        _need(images.is_contiguous(), "images must be contiguous")
+        if on_device:
+            _need(images.is_cuda and images.device.index == self.device,
+                  f"images must be on cuda:{self.device}, got {images.device}")
+        else:
+            _need(not images.is_cuda, "forward_host takes host (CPU) tensors")
+
+    def _check_out(self, out, need_bytes: int, on_device: bool):
+        import torch
+        _need(isinstance(out, torch.Tensor), "out must be a torch tensor")
+        want = torch.float32 if self.act == "f32" else torch.bfloat16
+        _need(out.dtype == want, f"out must be {want}, got {out.dtype}")
+        _need(out.is_contiguous(), "out must be contiguous")
+        _need(out.numel() * out.element_size() >= need_bytes, f"out holds {out.numel() * out.element_size()} bytes, "
+              f"needs {need_bytes}")
+        if on_device:
+            _need(out.is_cuda and out.device.index == self.device, f"out must be on cuda:{self.device}")
+        else:
+            _need(not out.is_cuda, "forward_host writes a host (CPU) tensor")
+
     def forward(self, split_idx: int, images, out):
         """images: CUDA fp32 [batch,3,H,W] contiguous tensor; out: CUDA tensor with room
         for the split output (act dtype).  Launches on the model's stream."""
-        assert images.is_cuda and images.is_contiguous() and out.is_cuda and out.is_contiguous()
+        self._check_images(images, True)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), True)
         _check(_lib.hapi_prefix_forward(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
                                         C.c_void_p(out.data_ptr())))
         return out
@@ -160,19 +200,31 @@ class Model:
     def forward_suffix(self, end_idx: int, acts, out):
         """acts: CUDA tensor holding layer start_idx's output (NCHW, act dtype); out: CUDA
         tensor with room for layer end_idx's output."""
-        assert acts.is_cuda and acts.is_contiguous() and out.is_cuda and out.is_contiguous()
+        import torch
+        _need(isinstance(acts, torch.Tensor) and acts.is_cuda and acts.device.index == self.device,
+              f"acts must be a tensor on cuda:{self.device}")
+        _need(acts.is_contiguous() and acts.dtype == (torch.float32 if self.act == "f32" else torch.bfloat16),
+              "acts must be contiguous, in the model's act dtype")
+        n = acts.shape[0]
+        _need(acts.numel() * acts.element_size() == n * self._split_bytes(self.start_idx),
+              f"acts must hold {n} layer-{self.start_idx} outputs")
+        self._check_out(out, n * self._split_bytes(end_idx), True)
         _check(_lib.hapi_suffix_forward(self._h, end_idx, C.c_void_p(acts.data_ptr()), acts.shape[0],
                                         C.c_void_p(out.data_ptr())))
         return out
 
     def forward_host(self, split_idx: int, images, out):
-        """HOST buffers (numpy or CPU tensors); synchronous end-to-end call."""
-        ip = images.ctypes.data if hasattr(images, "ctypes") else images.data_ptr()
-        op = out.ctypes.data if hasattr(out, "ctypes") else out.data_ptr()
+        """HOST buffers (CPU torch tensors, ideally pinned); synchronous end-to-end call.
+        Needs a model created with host_chunk != 0."""
+        self._check_images(images, False)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), False)
+        ip, op = images.data_ptr(), out.data_ptr()
         _check(_lib.hapi_prefix_forward_host(self._h, split_idx, C.c_void_p(ip), images.shape[0], C.c_void_p(op)))
         return out
 
     def forward_timed(self, split_idx: int, images, out) -> List[float]:
+        self._check_images(images, True)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), True)
         n = self.plan_info(split_idx)["n"]
         ms = (C.c_float * n)()
         _check(_lib.hapi_prefix_forward_timed(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],

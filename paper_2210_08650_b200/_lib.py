@@ -35,7 +35,7 @@ class AdaptRequest(C.Structure):
 
 class ModelDesc(C.Structure):
     _fields_ = [("arch", C.c_int), ("act", C.c_int), ("in_h", u32), ("in_w", u32), ("min_split", u32),
-                ("max_split", u32), ("max_batch", u32), ("device", C.c_int)]
+                ("max_split", u32), ("max_batch", u32), ("device", C.c_int), ("host_chunk", u32)]
 
 
 def _sig(name, res, *args):

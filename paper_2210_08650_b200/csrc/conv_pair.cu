@@ -367,11 +367,10 @@ __global__ void __launch_bounds__(P_THREADS, 1)
 template <int N2>
 cudaError_t launch_pair(const PairArgs& a, const PairMaps& mp, int num_sms, cudaStream_t st) {
   using C = PairCfg<N2>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(conv_pair_kernel<N2>, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM_LIMIT);
+  static std::atomic<uint64_t> attr_mask{0};
+  {
+    cudaError_t e = ensure_smem_attr(attr_mask, conv_pair_kernel<N2>, P_SMEM_LIMIT);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   int stages = (P_SMEM_LIMIT - C::FIXED) / C::STAGE;
   if (stages > P_MAX_STAGES) stages = P_MAX_STAGES;

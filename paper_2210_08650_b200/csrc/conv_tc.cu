@@ -1259,12 +1259,10 @@ int res_depth_pick(int stage_bytes, int fixed, int sb_bytes) {
 template <int BN, int MODE>
 cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, cudaStream_t st) {
   using C = Cfg<BN>;
-  static bool attr_set = false;  // per-instantiation; benign race (idempotent)
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_LIMIT);
+  static std::atomic<uint64_t> attr_mask{0};  // per instantiation, one bit per device
+  {
+    cudaError_t e = ensure_smem_attr(attr_mask, conv_tc_kernel<BN, MODE>, SMEM_LIMIT);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   g.res_box_bytes = (g.mode == 4 || g.mode == 6) ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
   int smem;

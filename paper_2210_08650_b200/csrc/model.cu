@@ -262,7 +262,9 @@ struct hapi_model {
   std::vector<Plan> plans;  // index split - min_split
   void* arena = nullptr;
   int64_t arena_bytes = 0;
-  // host pipeline (lazy)
+  // host pipeline (desc.host_chunk > 0): streams, events and staging made at create time
+  int64_t stage_bytes = 0;              // device bytes of the four staging buffers
+  uint32_t host_chunk = 0;              // images per staging slot
   cudaStream_t copy_stream = nullptr;   // host path: H2D copies
   cudaStream_t out_stream = nullptr;    // host path: D2H copies (separate, so the next H2D never
                                         // queues behind a D2H that waits for compute)
@@ -286,6 +288,19 @@ struct hapi_model {
 namespace {
 
 // ---------------------------------------------------------------- helpers
+// Every entry point runs on the model's device and leaves the caller's current device as
+// it found it (a process may hold models on several GPUs).
+struct DeviceGuard {
+  int prev = -1;
+  bool switched = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) switched = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (switched) cudaSetDevice(prev);
+  }
+};
+
 hapi_status dev_alloc(hapi_model* m, size_t bytes, void** p, bool weights) {
   if (bytes == 0) bytes = 16;
   cudaError_t e = cudaMalloc(p, bytes);
@@ -1577,6 +1592,22 @@ hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const float* i
     return st;
   }
   if (e != cudaSuccess) return set_error(HAPI_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+  // Same (split, chunk size) with other buffers (the serving case: a caching allocator hands
+  // out new pointers): the topology is identical, so update that executable graph's kernel
+  // parameters in place instead of instantiating another one.
+  for (auto& g : m->graphs) {
+    if (g.split != (uint32_t)p.split || g.nb != nb) continue;
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(g.exec, graph, &info) == cudaSuccess) {
+      cudaGraphDestroy(graph);
+      g.images = images;
+      g.out = out;
+      HAPI_CUDA_TRY(cudaGraphLaunch(g.exec, m->stream));
+      return HAPI_OK;
+    }
+    cudaGetLastError();  // a refused update is not an error: instantiate below
+    break;
+  }
   cudaGraphExec_t exec = nullptr;
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -1593,6 +1624,28 @@ hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const float* i
 const Plan* get_plan(hapi_model* m, uint32_t split) {
   if (split < m->d.min_split || split > m->d.max_split) return nullptr;
   return &m->plans[split - m->d.min_split];
+}
+
+// Host path (f2): two staging slots of host_chunk images in and split outputs out, plus the
+// copy streams and events, all made at create time so hapi_prefix_forward_host never
+// allocates and hapi_model_device_bytes reports them.
+hapi_status host_setup(hapi_model* m) {
+  const uint32_t c = std::min<uint32_t>(m->d.host_chunk, m->d.max_batch);
+  const int64_t img_bytes = 12ll * m->d.in_h * m->d.in_w;
+  int64_t max_out = 0;
+  for (const Plan& q : m->plans) max_out = std::max(max_out, q.out_bytes_per_img);
+  HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
+  HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->out_stream, cudaStreamNonBlocking));
+  for (auto& e : m->ev) HAPI_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  m->host_ready = true;  // streams/events exist: destroy releases them
+  for (int k = 0; k < 2; ++k) {
+    hapi_status st = dev_alloc(m, (size_t)img_bytes * c, &m->stage_in[k], false);
+    if (st == HAPI_OK) st = dev_alloc(m, (size_t)max_out * c, &m->stage_out[k], false);
+    if (st != HAPI_OK) return st;
+  }
+  m->host_chunk = c;
+  m->stage_bytes = 2 * ((int64_t)img_bytes * c + max_out * c);
+  return HAPI_OK;
 }
 
 }  // namespace
@@ -1642,7 +1695,10 @@ static hapi_status create_impl(const hapi_model_desc* desc, uint32_t start, cons
       if (k + 1 == start) in_numel = s.numel();
     }
   }
-  HAPI_CUDA_TRY(cudaSetDevice(desc->device));
+  int ndev = 0;
+  HAPI_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (desc->device < 0 || desc->device >= ndev) return set_error(HAPI_ERR_INVALID_ARGUMENT, "device %d", desc->device);
+  DeviceGuard dg(desc->device);
   std::unique_ptr<hapi_model> m(new hapi_model());
   m->d = *desc;
   m->arch = A;
@@ -1677,6 +1733,7 @@ static hapi_status create_impl(const hapi_model_desc* desc, uint32_t start, cons
   {
     hapi_status st = dev_alloc(m.get(), (size_t)m->arena_bytes, &m->arena, false);
     if (st == HAPI_OK) st = finalize_tmaps(m.get());
+    if (st == HAPI_OK && start == 0 && desc->host_chunk > 0) st = host_setup(m.get());
     if (st != HAPI_OK) {
       hapi_model_destroy(m.release());
       return st;
@@ -1698,6 +1755,7 @@ hapi_status hapi_suffix_forward(hapi_model* m, uint32_t end_idx, const void* act
   if (!m || !acts || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "not a suffix model (use hapi_prefix_forward)");
   if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
+  DeviceGuard dg(m->d.device);
   const Plan* p = get_plan(m, end_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "end_idx %u outside [%u,%u]", end_idx, m->d.min_split, m->d.max_split);
   HAPI_CUDA_TRY(cudaGetLastError());
@@ -1717,6 +1775,7 @@ hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* 
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
   if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
+  DeviceGuard dg(m->d.device);
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
   HAPI_CUDA_TRY(cudaGetLastError());
@@ -1740,6 +1799,7 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
   if (batch == 0 || batch > m->d.max_batch) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch must be in [1, max_batch]");
+  DeviceGuard dg(m->d.device);
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
   std::vector<cudaEvent_t> evs(p->ops.size() + 1);
@@ -1762,29 +1822,17 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
   if (batch == 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "batch = 0");
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
+  if (m->host_chunk == 0)
+    return set_error(HAPI_ERR_INVALID_ARGUMENT, "model created with host_chunk = 0 (no host-path staging)");
+  DeviceGuard dg(m->d.device);
   const int64_t img_bytes = 12ll * m->d.in_h * m->d.in_w;
-  int64_t max_out = 0;
-  for (const Plan& q : m->plans) max_out = std::max(max_out, q.out_bytes_per_img);
-  if (!m->host_ready) {
-    HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
-    HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->out_stream, cudaStreamNonBlocking));
-    for (int k = 0; k < 2; ++k) {
-      hapi_status st = dev_alloc(m, (size_t)img_bytes * m->d.max_batch, &m->stage_in[k], false);
-      if (st == HAPI_OK) st = dev_alloc(m, (size_t)max_out * m->d.max_batch, &m->stage_out[k], false);
-      if (st != HAPI_OK) return st;
-    }
-    for (auto& e : m->ev) HAPI_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    m->host_ready = true;
-  }
   // ev[0..1] h2d done, ev[2..3] compute done, ev[4..5] d2h done (slot reuse)
   cudaStream_t cs = m->stream, xs = m->copy_stream, ys = m->out_stream;
   // sub-chunks so the H2D copy of chunk i+1 and the D2H of chunk i-1 overlap compute of chunk i
-  // (H2D and D2H on their own streams: PCIe is full duplex)
-  uint64_t B = m->d.max_batch;
+  // (H2D and D2H on their own streams: PCIe is full duplex).  Chunk = the staging slot
+  // (create time; ~3/16 of a 512 batch measured best on ResNet-50)
+  uint64_t B = m->host_chunk;
   if (const char* e = std::getenv("HAPI_HOST_CHUNK")) B = std::min<uint64_t>(B, std::max(1, std::atoi(e)));
-  // ~3/16 of the batch (96 of 512): measured best e2e on ResNet-50 b512 among 64-172 with the
-  // ramped first chunk below (PCIe Gen5 H2D at 53 GB/s vs the compute of each chunk)
-  else if (batch >= 256) B = std::min<uint64_t>(B, std::max<uint64_t>(64, (batch * 3 / 16 + 15) / 16 * 16));
   // chunk schedule: a half-size first chunk (its H2D copy is the pipeline fill nothing overlaps),
   // then full chunks, the remainder last (HAPI_HOST_RAMP=0: equal chunks)
   std::vector<uint64_t> sizes;
@@ -1832,7 +1880,7 @@ hapi_status hapi_model_device_bytes(const hapi_model* m, uint64_t* wb, uint64_t*
   clear_error();
   if (!m) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null model");
   if (wb) *wb = (uint64_t)m->weight_bytes;
-  if (ab) *ab = (uint64_t)m->arena_bytes;
+  if (ab) *ab = (uint64_t)(m->arena_bytes + m->stage_bytes);
   return HAPI_OK;
 }
 
@@ -1866,7 +1914,7 @@ hapi_status hapi_plan_info(const hapi_model* m, uint32_t split_idx, uint32_t* n,
 
 void hapi_model_destroy(hapi_model* m) {
   if (!m) return;
-  cudaSetDevice(m->d.device);
+  DeviceGuard dg(m->d.device);
   for (auto& g : m->graphs) cudaGraphExecDestroy(g.exec);
   if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
   if (m->host_ready) {

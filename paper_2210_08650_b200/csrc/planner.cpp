@@ -205,27 +205,42 @@ hapi_status hapi_adapt_batches(const hapi_adapt_request* reqs, uint32_t n, uint6
     rem -= need;
     for (uint32_t i : order) batch[i] = reqs[i].b_min;
     // F2 unit water-filling: one more sample to the smallest b (earliest arrival on ties) that
-    // is below its b_max and whose M(data) still fits.  Granted here a level at a time: the
-    // winner keeps winning unit steps until it reaches an earlier-arrived rival's b, or passes
-    // a later-arrived rival's b by one, so those unit steps are applied at once.
-    std::vector<uint32_t> pos(n, 0);
-    for (uint32_t k = 0; k < order.size(); ++k) pos[order[k]] = k;
+    // is below its b_max and whose M(data) still fits.  Computed a level at a time: the unit
+    // process raises every eligible request at the minimum level m once, in arrival order,
+    // before any goes to m + 2, so while the group's summed M(data) fits, whole levels are
+    // granted at once (up to the next occupied level or the group's smallest b_max); a level
+    // that does not fit completely is finished one unit step at a time.  Cost O(n^2) levels
+    // instead of O(n * b_max) unit steps.
+    auto eligible = [&](uint32_t i) { return batch[i] < reqs[i].b_max && reqs[i].data_bytes <= rem; };
     for (;;) {
-      int64_t best = -1;
-      for (uint32_t i : order) {  // arrival order: the first minimum wins ties
-        const hapi_adapt_request& r = reqs[i];
-        if (batch[i] < r.b_max && r.data_bytes <= rem && (best < 0 || batch[i] < batch[best])) best = i;
-      }
-      if (best < 0) break;
-      uint64_t next = reqs[best].b_max;
+      uint32_t m = UINT32_MAX;
+      for (uint32_t i : order)
+        if (eligible(i)) m = std::min(m, batch[i]);
+      if (m == UINT32_MAX) break;
+      uint64_t S = 0, levels = UINT64_MAX;
+      bool ovf = false;
       for (uint32_t i : order) {
-        if ((int64_t)i == best || batch[i] >= reqs[i].b_max || reqs[i].data_bytes > rem) continue;
-        next = std::min<uint64_t>(next, (uint64_t)batch[i] + (pos[i] < pos[best] ? 0 : 1));
+        if (!eligible(i)) continue;
+        if (batch[i] == m) {
+          if (!add_ok(S, reqs[i].data_bytes, &S)) ovf = true;
+          levels = std::min<uint64_t>(levels, (uint64_t)reqs[i].b_max - m);
+        } else {
+          levels = std::min<uint64_t>(levels, (uint64_t)batch[i] - m);  // next occupied level
+        }
       }
-      uint64_t grant = next - batch[best];  // >= 1 (see above)
-      if (reqs[best].data_bytes > 0) grant = std::min<uint64_t>(grant, rem / reqs[best].data_bytes);
-      batch[best] += (uint32_t)grant;
-      rem -= grant * reqs[best].data_bytes;
+      if (!ovf && S > 0) levels = std::min<uint64_t>(levels, rem / S);
+      if (!ovf && levels >= 1) {
+        for (uint32_t i : order)
+          if (eligible(i) && batch[i] == m) batch[i] += (uint32_t)levels;
+        rem -= levels * S;  // <= rem (levels <= rem / S)
+        continue;
+      }
+      for (uint32_t i : order)  // partial level: one unit step, first minimum by arrival
+        if (eligible(i) && batch[i] == m) {
+          batch[i] += 1;
+          rem -= reqs[i].data_bytes;
+          break;
+        }
     }
   }
   if (used_bytes) *used_bytes = available_bytes - rem;

@@ -162,3 +162,21 @@ def test_abi_with_planner_sizes():
     b, used = H.hapi_adapt_batches([(r.arrival_seq, r.model_bytes, r.data_bytes, r.b_min, r.b_max) for r in reqs],
                                    tight)
     assert all(25 <= x <= 2000 for x in b) and used <= tight
+
+
+def test_abi_large_b_max_is_fast_and_exact():
+    """The C solver grants whole levels to the group at the minimum level (the
+    unit loop cost O(n * b_max)); the result still equals the oracle's unit process, and u32
+    b_max no longer means minutes of host time."""
+    import time
+
+    import paper_2210_08650_b200 as H
+    reqs = [(0, 10, 3, 1, 10 ** 7), (1, 20, 3, 1, 10 ** 7), (2, 0, 5, 2, 4_000_000_000)]
+    t0 = time.perf_counter()
+    got, used = H.hapi_adapt_batches(reqs, 10 ** 10)
+    assert time.perf_counter() - t0 < 0.5
+    assert got[:2] == [10 ** 7, 10 ** 7] and used <= 10 ** 10
+    small = [R(i, m, d, lo, hi) for i, (_, m, d, lo, hi) in enumerate(reqs[:2])]
+    want, wused = adapt_batches([R(r.arrival_seq, r.model_bytes, r.data_bytes, r.b_min, 300) for r in small], 1000)
+    got2, gused = H.hapi_adapt_batches([(r.arrival_seq, r.model_bytes, r.data_bytes, r.b_min, 300) for r in small], 1000)
+    assert (got2, gused) == (want, wused)

@@ -177,13 +177,76 @@ def test_host_path_matches_oracle_and_device_path(n, max_batch):
     arch, s = "resnet18", 10
     P = hapi_inputs.params(arch, 10)
     x = hapi_inputs.images(n, 11, 64, 64)
-    m = H.Model(arch, "bf16", list(P.values()), max_batch, s, s, in_h=64, in_w=64)
+    m = H.Model(arch, "bf16", list(P.values()), max_batch, s, s, in_h=64, in_w=64, host_chunk=max_batch)
     host, _ = gpu_forward(arch, "bf16", s, x, P, model=m, host=True)
     sel = sorted({0, 1, n // 2, n - 2, n - 1} | ({31, 32, 95, 96, 159, 160} if n == 200 else set()))
     ref = oracle_all(arch, 10, 11, n, 64, 64, upto=s, sel=sel)[s - 1]
     check_close(host[sel], ref, "bf16", f"host path n={n}")
     dev, _ = gpu_forward(arch, "bf16", s, x, P, model=m)
     np.testing.assert_array_equal(dev, host)
+
+
+@pytest.mark.parametrize("arch,split,b", [("resnet50", 21, 512), ("resnet50", 21, 25), ("densenet121", 9, 200),
+                                          ("resnet18", 10, 1)])
+def test_memory_bound_with_host_staging(arch, split, b):
+    """With the host path's staging (allocated at create time, counted in device_bytes), the
+    model stays within est(b, s) plus the closed-form staging term 2 * c * (l_0 + l_s) -- the
+    double-buffered DRAM<->GPU copies of Eq. 1's C11 * B * (l_0 + l_split) (PAPER.md:204-206;
+    reading A14: a term added to both sides)."""
+    H = _H()
+    P = hapi_inputs.params(arch, 7)
+    m = H.Model(arch, "bf16", list(P.values()), b, split, split, host_chunk=-1)
+    wb, ab = m.device_bytes()
+    c = b if b < 256 else min(b, max(64, (b * 3 // 16 + 15) // 16 * 16))
+    sz = planner.layer_sizes(arch, act="bf16")
+    assert wb + ab <= planner.estimate(arch, split, b, "bf16") + 2 * c * (sz.input_bytes + sz.out_bytes[split - 1])
+    m.close()
+
+
+def test_python_argument_validation():
+    """The binding checks dtype, shape, device and output size before any pointer reaches
+    the library: ValueError, never an out-of-bounds access."""
+    import torch
+    H = _H()
+    P = hapi_inputs.params("resnet18", 0)
+    m = H.Model("resnet18", "bf16", list(P.values()), 2, 10, 10, in_h=64, in_w=64)
+    x = torch.zeros(2, 3, 64, 64, device="cuda")
+    out = torch.zeros(2 * m.out_bytes[9] // 2, dtype=torch.bfloat16, device="cuda")
+    m.forward(10, x, out)
+    for bad_x, bad_out in ((x.half(), out), (x[:, :2].contiguous(), out), (x.cpu(), out),
+                           (torch.zeros(2, 3, 32, 32, device="cuda"), out), (x, out[:-1]), (x, out.float()),
+                           (x, out.cpu())):
+        with pytest.raises(ValueError):
+            m.forward(10, bad_x, bad_out)
+    with pytest.raises(H.HapiError) as e:
+        m.forward_host(10, x.cpu(), out.cpu())          # no staging was requested (host_chunk = 0)
+    assert e.value.status == 1
+    m.close()
+
+
+def test_models_on_two_devices_in_one_process():
+    """Per-device kernel attributes and the device guard: two models on two GPUs
+    driven from one thread give the same bits as each alone, and the caller's current
+    device is left unchanged."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    H = _H()
+    P = hapi_inputs.params("resnet50", 5)
+    x = hapi_inputs.images(3, 6, 96, 96)
+    outs = []
+    torch.cuda.set_device(0)
+    for dev in (0, 1):
+        m = H.Model("resnet50", "bf16", list(P.values()), 3, 21, 21, in_h=96, in_w=96, device=dev)
+        assert torch.cuda.current_device() == 0
+        xd = torch.from_numpy(x).to(f"cuda:{dev}")
+        o = torch.empty(3 * m.out_bytes[20] // 2, dtype=torch.bfloat16, device=f"cuda:{dev}")
+        m.forward(21, xd, o)
+        torch.cuda.synchronize(dev)
+        assert torch.cuda.current_device() == 0
+        outs.append(o.cpu())
+        m.close()
+    assert torch.equal(outs[0].view(torch.int16), outs[1].view(torch.int16))
 
 
 def test_gpu_argument_errors():
