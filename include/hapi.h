@@ -149,6 +149,49 @@ HAPI_API hapi_status hapi_adapt_batches(const hapi_adapt_request *reqs, uint32_t
  * INVALID_ARGUMENT (n_gpus = 0, null gpu_of with n > 0). */
 HAPI_API hapi_status hapi_partition_requests(uint32_t n, uint32_t n_gpus, uint32_t *gpu_of);
 
+/* ------------------------------------------------------------------ server loop (f1)
+ * The batch-adaptation loop of one GPU (section 4.5): requests are
+ * queued; a round of hapi_adapt_batches runs "when two conditions hold: (1) there is
+ * available GPU memory for new requests, and (2) there exists at least one queued request
+ * that has not yet been accounted for in the previous runs", after the server "waits for
+ * new requests for a small amount of time"; requests the round cannot fit "become part of
+ * the next batch assignment round, typically after some existing requests finish".
+ * Readings:
+ *   F5 the round runs at the first poll with now >= (earliest unaccounted arrival) + wait_us;
+ *   F6 available = total - occupied - sum over running requests of (W_r + b_r * P_r);
+ *      condition (1) = available > 0 and (no cap, or fewer running requests than the cap);
+ *   F7 a round considers the unaccounted and the deferred requests, with the static cap
+ *      reduced by the running count; admitted requests run, the others become deferred;
+ *   F8 hapi_scheduler_finish returns the request's memory and makes deferred requests
+ *      unaccounted again (original arrival times kept).
+ * Host-only, deterministic (the caller supplies the clock), not thread-safe per handle. */
+typedef struct hapi_scheduler hapi_scheduler;
+typedef enum { HAPI_REQ_QUEUED = 0, HAPI_REQ_DEFERRED = 1, HAPI_REQ_RUNNING = 2, HAPI_REQ_DONE = 3 } hapi_req_state;
+typedef struct {
+  uint64_t total_bytes;           /* M_total of the GPU */
+  uint64_t occupied_bytes;        /* M(occupied): CUDA/framework reservation estimated by the provider */
+  uint32_t max_concurrency;       /* static cap on running requests; 0 = none */
+  uint64_t wait_us;               /* the wait window (F5) */
+} hapi_scheduler_config;
+/* Errors: INVALID_ARGUMENT (null, occupied > total). */
+HAPI_API hapi_status hapi_scheduler_create(const hapi_scheduler_config *cfg, hapi_scheduler **out);
+/* Queue a request arriving at now_us (non-decreasing across calls): r->arrival_seq is ignored
+ * (arrival = now_us, ties by submission order); *id <- its handle (0, 1, 2, ...).
+ * Errors: INVALID_ARGUMENT (null, bad bounds, now_us earlier than a previous call). */
+HAPI_API hapi_status hapi_scheduler_submit(hapi_scheduler *s, uint64_t now_us, const hapi_adapt_request *r,
+                                           uint64_t *id);
+/* Run a round if the trigger holds at now_us: ids[k], batches[k] <- the admitted requests in
+ * arrival order (k < *n_admitted <= cap; a round admitting more than cap is an
+ * INVALID_ARGUMENT before any state change).  *n_admitted = 0 when no round ran. */
+HAPI_API hapi_status hapi_scheduler_poll(hapi_scheduler *s, uint64_t now_us, uint64_t *ids, uint32_t *batches,
+                                         uint32_t cap, uint32_t *n_admitted);
+/* A running request completed.  Errors: INVALID_ARGUMENT (unknown id, not running). */
+HAPI_API hapi_status hapi_scheduler_finish(hapi_scheduler *s, uint64_t id);
+/* State and COS batch (0 unless running) of request id; *available <- F6 available bytes. */
+HAPI_API hapi_status hapi_scheduler_query(const hapi_scheduler *s, uint64_t id, uint32_t *state, uint32_t *batch,
+                                          uint64_t *available);
+HAPI_API void hapi_scheduler_destroy(hapi_scheduler *s);
+
 /* Parameters expected by hapi_model_create, in torchvision state_dict order
  * (num_batches_tracked buffers excluded): count, and per index the name (copied into
  * name_buf, NUL-terminated, truncated to name_cap) and shape (dims[4], *ndim). */

@@ -96,6 +96,52 @@ def hapi_partition_requests(n: int, n_gpus: int):
     return list(out)[:n]
 
 
+class Scheduler:
+    """hapi_scheduler handle: the section 4.5 batch-adaptation loop of one GPU (host-only;
+    the caller supplies the clock in microseconds)."""
+
+    QUEUED, DEFERRED, RUNNING, DONE = 0, 1, 2, 3
+
+    def __init__(self, total_bytes: int, occupied_bytes: int = 0, max_concurrency: int = 0, wait_us: int = 0):
+        cfg = _lib.SchedulerConfig(total_bytes, occupied_bytes, max_concurrency, wait_us)
+        h = C.c_void_p()
+        _check(_lib.hapi_scheduler_create(C.byref(cfg), C.byref(h)))
+        self._h = h
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None and getattr(_lib, "hapi_scheduler_destroy", None) is not None:
+            _lib.hapi_scheduler_destroy(h)
+        self._h = None
+
+    __del__ = close
+
+    def submit(self, now_us: int, model_bytes: int, data_bytes: int, b_min: int, b_max: int) -> int:
+        rid = _lib.u64()
+        r = _lib.AdaptRequest(0, model_bytes, data_bytes, b_min, b_max)
+        _check(_lib.hapi_scheduler_submit(self._h, now_us, C.byref(r), C.byref(rid)))
+        return rid.value
+
+    def poll(self, now_us: int, cap: int = 4096):
+        """-> [(request id, COS batch)] admitted by a round at now_us ([] if none ran)."""
+        ids, bs, n = (_lib.u64 * cap)(), (_lib.u32 * cap)(), _lib.u32()
+        _check(_lib.hapi_scheduler_poll(self._h, now_us, ids, bs, cap, C.byref(n)))
+        return [(ids[i], bs[i]) for i in range(n.value)]
+
+    def finish(self, rid: int):
+        _check(_lib.hapi_scheduler_finish(self._h, rid))
+
+    def state(self, rid: int):
+        st, b = _lib.u32(), _lib.u32()
+        _check(_lib.hapi_scheduler_query(self._h, rid, C.byref(st), C.byref(b), None))
+        return st.value, b.value
+
+    def available(self) -> int:
+        a = _lib.u64()
+        _check(_lib.hapi_scheduler_query(self._h, 0, None, None, C.byref(a)))
+        return a.value
+
+
 def hapi_param_table(arch):
     """[(name, shape)] the library expects, in torchvision state_dict order."""
     n = _lib.hapi_num_params(_arch(arch))

@@ -67,6 +67,16 @@ hapi_prefix_forward_timed = _sig("hapi_prefix_forward_timed", C.c_int, C.c_void_
                                  P_f32, u32)
 hapi_plan_describe = _sig("hapi_plan_describe", C.c_int, C.c_void_p, u32, u32, C.c_char_p, u32)
 hapi_model_destroy = _sig("hapi_model_destroy", None, C.c_void_p)
+class SchedulerConfig(C.Structure):
+    _fields_ = [("total_bytes", u64), ("occupied_bytes", u64), ("max_concurrency", u32), ("wait_us", u64)]
+
+
+hapi_scheduler_create = _sig("hapi_scheduler_create", C.c_int, C.POINTER(SchedulerConfig), C.POINTER(C.c_void_p))
+hapi_scheduler_submit = _sig("hapi_scheduler_submit", C.c_int, C.c_void_p, u64, C.POINTER(AdaptRequest), P_u64)
+hapi_scheduler_poll = _sig("hapi_scheduler_poll", C.c_int, C.c_void_p, u64, P_u64, P_u32, u32, P_u32)
+hapi_scheduler_finish = _sig("hapi_scheduler_finish", C.c_int, C.c_void_p, u64)
+hapi_scheduler_query = _sig("hapi_scheduler_query", C.c_int, C.c_void_p, u64, P_u32, P_u32, P_u64)
+hapi_scheduler_destroy = _sig("hapi_scheduler_destroy", None, C.c_void_p)
 hapi_last_error = _sig("hapi_last_error", C.c_char_p)
 hapi_build_info = _sig("hapi_build_info", C.c_char_p)
 
@@ -74,4 +84,6 @@ EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_ch
             "hapi_partition_requests", "hapi_model_create_suffix", "hapi_suffix_forward", "hapi_num_params",
             "hapi_param_info", "hapi_model_create", "hapi_model_set_stream", "hapi_prefix_forward",
             "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_plan_describe", "hapi_prefix_forward_timed",
-            "hapi_model_destroy", "hapi_last_error", "hapi_build_info"]
+            "hapi_model_destroy", "hapi_last_error", "hapi_build_info", "hapi_scheduler_create",
+            "hapi_scheduler_submit", "hapi_scheduler_poll", "hapi_scheduler_finish", "hapi_scheduler_query",
+            "hapi_scheduler_destroy"]
