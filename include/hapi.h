@@ -200,6 +200,7 @@ HAPI_API hapi_status hapi_param_info(hapi_arch arch, uint32_t idx, char *name_bu
                             int64_t dims[4], uint32_t *ndim);
 
 /* ------------------------------------------------------------------ executor (device) */
+/* (the model API is below; the serving loop that drives it, hapi_server, follows it) */
 
 typedef struct hapi_model hapi_model;
 
@@ -229,6 +230,14 @@ typedef struct {
  * (n_params != hapi_num_params, unsupported image size), OUT_OF_MEMORY, CUDA. */
 HAPI_API hapi_status hapi_model_create(const hapi_model_desc *desc, const float *const *params,
                               uint32_t n_params, hapi_model **m);
+
+/* A model over the SAME device weights as `base` (no copy; the weights are freed with the
+ * last model that holds them), with its own plans, arena for max_batch images and host
+ * staging (host_chunk, 0 = none): concurrent requests of one (arch, split range) share one
+ * copy of the frozen weights (f1).  Its hapi_model_device_bytes reports 0 weight bytes (they
+ * are counted once, on the base).  Errors: INVALID_ARGUMENT, OUT_OF_MEMORY, CUDA. */
+HAPI_API hapi_status hapi_model_create_shared(const hapi_model *base, uint32_t max_batch, uint32_t host_chunk,
+                                              hapi_model **out);
 
 /* Stream for subsequent launches (a cudaStream_t; NULL = legacy default stream). */
 HAPI_API hapi_status hapi_model_set_stream(hapi_model *m, void *cuda_stream);
@@ -297,6 +306,43 @@ HAPI_API hapi_status hapi_prefix_forward_timed(hapi_model *m, uint32_t split_idx
                                       uint64_t batch, void *out, float *ms, uint32_t cap);
 
 HAPI_API void hapi_model_destroy(hapi_model *m);
+
+/* ------------------------------------------------------------------ serving loop (f1, device)
+ * The HAPI server of one GPU (section 4.5): frozen models are registered
+ * once (their weights shared by every request), requests are queued with their device
+ * images and output buffers, and each hapi_server_step (1) retires requests whose forward
+ * has completed (hapi_scheduler_finish), (2) runs the scheduler (trigger, wait window,
+ * Eq. 4 round) and (3) launches every admitted request on its own stream: a model sharing
+ * the registered weights with an arena for its COS batch b_r, hapi_prefix_forward over the
+ * request's images in chunks of b_r.  Eq. 4 sizes per request are W(s), P(s) of
+ * hapi_layer_sizes (M_r(model), M_r(data)); b_max is the request's (the client's training
+ * batch) and b_min the provider's (25 in the paper; clipped to
+ * b_max).  Not thread-safe per handle. */
+typedef struct hapi_server hapi_server;
+typedef struct {
+  hapi_scheduler_config sched;    /* memory model, static cap, wait window */
+  int device;                     /* CUDA ordinal */
+  uint32_t b_min;                 /* provider's minimum COS batch */
+} hapi_server_config;
+HAPI_API hapi_status hapi_server_create(const hapi_server_config *cfg, hapi_server **out);
+/* Register a frozen model (desc->max_batch, host_chunk are ignored); *model_id <- its handle.
+ * Requests may use any split in [desc->min_split, desc->max_split]. */
+HAPI_API hapi_status hapi_server_add_model(hapi_server *s, const hapi_model_desc *desc, const float *const *params,
+                                           uint32_t n_params, uint32_t *model_id);
+/* Queue a request at now_us: `n` device images [n,3,H,W] fp32 -> device `out` (n * l_split
+ * bytes, contiguous NCHW, as hapi_prefix_forward); both owned by the caller and untouched
+ * until the request is DONE.  *req_id <- its handle. */
+HAPI_API hapi_status hapi_server_submit(hapi_server *s, uint64_t now_us, uint32_t model_id, uint32_t split_idx,
+                                        uint32_t b_max, const float *images, uint64_t n, void *out,
+                                        uint64_t *req_id);
+/* One iteration of the loop at now_us (see above).  *n_active <- requests not yet DONE. */
+HAPI_API hapi_status hapi_server_step(hapi_server *s, uint64_t now_us, uint32_t *n_active);
+/* State (hapi_req_state) and COS batch of a request; *device_bytes (may be NULL) <- bytes the
+ * server holds on the device right now (registered weights + running requests' arenas). */
+HAPI_API hapi_status hapi_server_query(const hapi_server *s, uint64_t req_id, uint32_t *state, uint32_t *batch,
+                                       uint64_t *device_bytes);
+/* Waits for running requests, then frees everything. */
+HAPI_API void hapi_server_destroy(hapi_server *s);
 
 /* Thread-local message describing the last error on this thread ("" if none). */
 HAPI_API const char *hapi_last_error(void);

@@ -142,6 +142,66 @@ class Scheduler:
         return a.value
 
 
+class Server:
+    """hapi_server handle: the section 4.5 serving loop of one GPU.  Requests carry device
+    tensors (kept alive here until the request is DONE)."""
+
+    def __init__(self, total_bytes: int, occupied_bytes: int = 0, max_concurrency: int = 0, wait_us: int = 0,
+                 device: int = 0, b_min: int = 25):
+        cfg = _lib.ServerConfig(_lib.SchedulerConfig(total_bytes, occupied_bytes, max_concurrency, wait_us), device,
+                                b_min)
+        h = C.c_void_p()
+        _check(_lib.hapi_server_create(C.byref(cfg), C.byref(h)))
+        self._h, self.device, self._keep = h, device, {}
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None and getattr(_lib, "hapi_server_destroy", None) is not None:
+            _lib.hapi_server_destroy(h)
+        self._h = None
+        self._keep = {}
+
+    __del__ = close
+
+    def add_model(self, arch, act, params: Sequence, min_split: int, max_split: int, in_h: int = 224,
+                  in_w: int = 224) -> int:
+        import numpy as np
+        keep = [np.ascontiguousarray(np.asarray(p, dtype=np.float32)) for p in params]
+        ptrs = (C.c_void_p * len(keep))(*[p.ctypes.data for p in keep])
+        d = _lib.ModelDesc(_arch(arch), _dt(act), in_h, in_w, min_split, max_split, 1, self.device, 0)
+        mid = _lib.u32()
+        _check(_lib.hapi_server_add_model(self._h, C.byref(d), ptrs, len(keep), C.byref(mid)))
+        return mid.value
+
+    def submit(self, now_us: int, model_id: int, split_idx: int, b_max: int, images, out) -> int:
+        import torch
+        _need(isinstance(images, torch.Tensor) and images.is_cuda and images.is_contiguous()
+              and images.dtype == torch.float32 and images.dim() == 4, "images: contiguous CUDA fp32 [N,3,H,W]")
+        _need(isinstance(out, torch.Tensor) and out.is_cuda and out.is_contiguous(), "out: contiguous CUDA tensor")
+        rid = _lib.u64()
+        _check(_lib.hapi_server_submit(self._h, now_us, model_id, split_idx, b_max, C.c_void_p(images.data_ptr()),
+                                       images.shape[0], C.c_void_p(out.data_ptr()), C.byref(rid)))
+        self._keep[rid.value] = (images, out)
+        return rid.value
+
+    def step(self, now_us: int) -> int:
+        n = _lib.u32()
+        _check(_lib.hapi_server_step(self._h, now_us, C.byref(n)))
+        for rid in [r for r in self._keep if self.state(r)[0] == Scheduler.DONE]:
+            del self._keep[rid]
+        return n.value
+
+    def state(self, rid: int):
+        st, b = _lib.u32(), _lib.u32()
+        _check(_lib.hapi_server_query(self._h, rid, C.byref(st), C.byref(b), None))
+        return st.value, b.value
+
+    def device_bytes(self) -> int:
+        t = _lib.u64()
+        _check(_lib.hapi_server_query(self._h, 0, None, None, C.byref(t)))
+        return t.value
+
+
 def hapi_param_table(arch):
     """[(name, shape)] the library expects, in torchvision state_dict order."""
     n = _lib.hapi_num_params(_arch(arch))
@@ -189,6 +249,16 @@ class Model:
         self._h = h
         self.device = device
         self.out_bytes = hapi_layer_sizes(arch, in_h, in_w, act)[1]
+
+    def shared(self, max_batch: int, host_chunk: int = 0) -> "Model":
+        """hapi_model_create_shared: a model over this model's device weights (no copy) with
+        its own arena for max_batch images -- one per concurrent request."""
+        h = C.c_void_p()
+        _check(_lib.hapi_model_create_shared(self._h, max_batch, host_chunk, C.byref(h)))
+        m = object.__new__(Model)
+        m.__dict__.update({k: v for k, v in self.__dict__.items() if k != "_h"})
+        m.max_batch, m._h = max_batch, h
+        return m
 
     def close(self):
         h = getattr(self, "_h", None)

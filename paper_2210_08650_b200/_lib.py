@@ -58,6 +58,7 @@ hapi_model_create = _sig("hapi_model_create", C.c_int, C.POINTER(ModelDesc), C.P
 hapi_model_create_suffix = _sig("hapi_model_create_suffix", C.c_int, C.POINTER(ModelDesc), u32, C.POINTER(C.c_void_p),
                                 u32, C.POINTER(C.c_void_p))
 hapi_suffix_forward = _sig("hapi_suffix_forward", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
+hapi_model_create_shared = _sig("hapi_model_create_shared", C.c_int, C.c_void_p, u32, u32, C.POINTER(C.c_void_p))
 hapi_model_set_stream = _sig("hapi_model_set_stream", C.c_int, C.c_void_p, C.c_void_p)
 hapi_prefix_forward = _sig("hapi_prefix_forward", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
 hapi_prefix_forward_host = _sig("hapi_prefix_forward_host", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
@@ -77,6 +78,18 @@ hapi_scheduler_poll = _sig("hapi_scheduler_poll", C.c_int, C.c_void_p, u64, P_u6
 hapi_scheduler_finish = _sig("hapi_scheduler_finish", C.c_int, C.c_void_p, u64)
 hapi_scheduler_query = _sig("hapi_scheduler_query", C.c_int, C.c_void_p, u64, P_u32, P_u32, P_u64)
 hapi_scheduler_destroy = _sig("hapi_scheduler_destroy", None, C.c_void_p)
+class ServerConfig(C.Structure):
+    _fields_ = [("sched", SchedulerConfig), ("device", C.c_int), ("b_min", u32)]
+
+
+hapi_server_create = _sig("hapi_server_create", C.c_int, C.POINTER(ServerConfig), C.POINTER(C.c_void_p))
+hapi_server_add_model = _sig("hapi_server_add_model", C.c_int, C.c_void_p, C.POINTER(ModelDesc), C.POINTER(C.c_void_p),
+                             u32, P_u32)
+hapi_server_submit = _sig("hapi_server_submit", C.c_int, C.c_void_p, u64, u32, u32, u32, C.c_void_p, u64, C.c_void_p,
+                          P_u64)
+hapi_server_step = _sig("hapi_server_step", C.c_int, C.c_void_p, u64, P_u32)
+hapi_server_query = _sig("hapi_server_query", C.c_int, C.c_void_p, u64, P_u32, P_u32, P_u64)
+hapi_server_destroy = _sig("hapi_server_destroy", None, C.c_void_p)
 hapi_last_error = _sig("hapi_last_error", C.c_char_p)
 hapi_build_info = _sig("hapi_build_info", C.c_char_p)
 
@@ -86,4 +99,5 @@ EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_ch
             "hapi_prefix_forward_host", "hapi_model_device_bytes", "hapi_plan_info", "hapi_plan_describe", "hapi_prefix_forward_timed",
             "hapi_model_destroy", "hapi_last_error", "hapi_build_info", "hapi_scheduler_create",
             "hapi_scheduler_submit", "hapi_scheduler_poll", "hapi_scheduler_finish", "hapi_scheduler_query",
-            "hapi_scheduler_destroy"]
+            "hapi_scheduler_destroy", "hapi_model_create_shared", "hapi_server_create", "hapi_server_add_model",
+            "hapi_server_submit", "hapi_server_step", "hapi_server_query", "hapi_server_destroy"]

@@ -242,8 +242,23 @@ struct Plan {
 
 }  // namespace
 
+// Device weights (packed convs, bias/BN vectors, the identity block) of a model, shared by
+// the models made from it with hapi_model_create_shared; freed with the last of them.
+struct WeightStore {
+  int device = 0;
+  std::vector<void*> ptrs;
+  ~WeightStore() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    if (prev != device) cudaSetDevice(device);
+    for (void* p : ptrs) cudaFree(p);
+    if (prev >= 0 && prev != device) cudaSetDevice(prev);
+  }
+};
+
 struct hapi_model {
   hapi_model_desc d;
+  std::shared_ptr<WeightStore> wstore;  // owned (or shared) weight allocations
   const ArchDesc* arch = nullptr;
   bool bf16 = true;
   int es = 2;
@@ -307,8 +322,12 @@ hapi_status dev_alloc(hapi_model* m, size_t bytes, void** p, bool weights) {
   if (e != cudaSuccess)
     return set_error(e == cudaErrorMemoryAllocation ? HAPI_ERR_OUT_OF_MEMORY : HAPI_ERR_CUDA, "cudaMalloc(%zu): %s", bytes,
                      cudaGetErrorString(e));
-  m->allocs.push_back(*p);
-  if (weights) m->weight_bytes += (int64_t)bytes;
+  if (weights) {
+    m->wstore->ptrs.push_back(*p);
+    m->weight_bytes += (int64_t)bytes;
+  } else {
+    m->allocs.push_back(*p);
+  }
   return HAPI_OK;
 }
 
@@ -332,6 +351,7 @@ uint16_t f2bf(float f) {  // round-to-nearest-even
 }
 
 const float* P(hapi_model* m, const std::string& name, int64_t expect_numel) {
+  if (m->host_params.empty()) return nullptr;  // a shared-weight model finds every conv in the cache
   int i = m->arch->find_param(name);
   if (i < 0) return nullptr;
   if (m->arch->params[i].numel() != expect_numel) return nullptr;
@@ -1648,6 +1668,25 @@ hapi_status host_setup(hapi_model* m) {
   return HAPI_OK;
 }
 
+// One launch plan per split in [min_split, max_split] (two candidates each: pool written
+// straight into the DenseNet block buffer, or through a compact buffer + copy; the smaller
+// arena is kept), then the arena, the TMA descriptors over it and the host-path staging.
+hapi_status plans_and_arena(hapi_model* m) {
+  for (uint32_t s = m->d.min_split; s <= m->d.max_split; ++s) {
+    Plan p, p2;
+    hapi_status st = build_plan(m, (int)s, &p, true);
+    if (st == HAPI_OK) st = build_plan(m, (int)s, &p2, false);
+    if (st != HAPI_OK) return st;
+    if (p2.arena_bytes < p.arena_bytes) p = std::move(p2);
+    m->arena_bytes = std::max(m->arena_bytes, p.arena_bytes);
+    m->plans.push_back(std::move(p));
+  }
+  hapi_status st = dev_alloc(m, (size_t)m->arena_bytes, &m->arena, false);
+  if (st == HAPI_OK) st = finalize_tmaps(m);
+  if (st == HAPI_OK && m->start == 0 && m->d.host_chunk > 0) st = host_setup(m);
+  return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1700,6 +1739,8 @@ static hapi_status create_impl(const hapi_model_desc* desc, uint32_t start, cons
   if (desc->device < 0 || desc->device >= ndev) return set_error(HAPI_ERR_INVALID_ARGUMENT, "device %d", desc->device);
   DeviceGuard dg(desc->device);
   std::unique_ptr<hapi_model> m(new hapi_model());
+  m->wstore = std::make_shared<WeightStore>();
+  m->wstore->device = desc->device;
   m->d = *desc;
   m->arch = A;
   m->bf16 = desc->act == HAPI_BF16;
@@ -1715,29 +1756,43 @@ static hapi_status create_impl(const hapi_model_desc* desc, uint32_t start, cons
       return set_error(HAPI_ERR_UNSUPPORTED, "bf16 tcgen05 path is built for sm_100a; device is sm_%d%d", major, minor);
   }
   m->host_params.assign(params, params + n_params);
-  for (uint32_t s = desc->min_split; s <= desc->max_split; ++s) {
-    // two candidate plans: pool written straight into the DenseNet block buffer (fewer
-    // launches) or through a compact buffer + copy (lower peak); keep the smaller arena
-    Plan p, p2;
-    hapi_status st = build_plan(m.get(), (int)s, &p, true);
-    if (st == HAPI_OK) st = build_plan(m.get(), (int)s, &p2, false);
-    if (st != HAPI_OK) {
-      hapi_model_destroy(m.release());
-      return st;
-    }
-    if (p2.arena_bytes < p.arena_bytes) p = std::move(p2);
-    m->arena_bytes = std::max(m->arena_bytes, p.arena_bytes);
-    m->plans.push_back(std::move(p));
-  }
+  hapi_status st = plans_and_arena(m.get());
   m->host_params.clear();
-  {
-    hapi_status st = dev_alloc(m.get(), (size_t)m->arena_bytes, &m->arena, false);
-    if (st == HAPI_OK) st = finalize_tmaps(m.get());
-    if (st == HAPI_OK && start == 0 && desc->host_chunk > 0) st = host_setup(m.get());
-    if (st != HAPI_OK) {
-      hapi_model_destroy(m.release());
-      return st;
-    }
+  if (st != HAPI_OK) {
+    hapi_model_destroy(m.release());
+    return st;
+  }
+  *out = m.release();
+  return HAPI_OK;
+}
+
+hapi_status hapi_model_create_shared(const hapi_model* base, uint32_t max_batch, uint32_t host_chunk, hapi_model** out) {
+  clear_error();
+  if (!base || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (max_batch < 1) return set_error(HAPI_ERR_INVALID_ARGUMENT, "max_batch = 0");
+  DeviceGuard dg(base->d.device);
+  std::unique_ptr<hapi_model> m(new hapi_model());
+  m->wstore = base->wstore;  // weights shared, freed with the last model holding them
+  m->d = base->d;
+  m->d.max_batch = max_batch;
+  m->d.host_chunk = host_chunk;
+  m->arch = base->arch;
+  m->bf16 = base->bf16;
+  m->es = base->es;
+  m->num_sms = base->num_sms;
+  m->start = base->start;
+  m->in_bytes_per_img = base->in_bytes_per_img;
+  m->convs = base->convs;            // device pointers into the shared store
+  m->conv_index = base->conv_index;  // every conv of the plans is found here (no host params)
+  m->bn_cache = base->bn_cache;
+  m->ident = base->ident;
+  m->ident_map128 = base->ident_map128;
+  m->ident_map256 = base->ident_map256;
+  hapi_status st = plans_and_arena(m.get());
+  if (st != HAPI_OK) {
+    hapi_model_destroy(m.release());
+    return st;
   }
   *out = m.release();
   return HAPI_OK;
