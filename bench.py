@@ -176,6 +176,35 @@ def run_reference(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def pin_to_gpu_numa_node(local: int):
+    """Bind this rank to the host cores of its GPU's NUMA node (sysfs local_cpulist of the
+    GPU's PCI function), so the pinned host buffers of the e2e leg are first-touched on the
+    node next to the GPU's PCIe root.  Returns the core list used (or None)."""
+    try:
+        import torch
+        bus = torch.cuda.get_device_properties(local).pci_bus_id if hasattr(
+            torch.cuda.get_device_properties(local), "pci_bus_id") else None
+        if bus is None:
+            out = subprocess.run(["nvidia-smi", f"--id={local}", "--query-gpu=pci.bus_id", "--format=csv,noheader"],
+                                 capture_output=True, text=True).stdout.strip()
+            bus = out
+        bus = bus.lower()
+        if bus.count(":") == 2 and len(bus.split(":")[0]) == 8:
+            bus = bus[4:]                       # 00000000:1b:00.0 -> 0000:1b:00.0
+        txt = open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+        cores = set()
+        for part in txt.split(","):
+            a, _, b = part.partition("-")
+            cores.update(range(int(a), int(b or a) + 1))
+        cores &= os.sched_getaffinity(0)
+        if cores:
+            os.sched_setaffinity(0, cores)
+            return sorted(cores)
+    except Exception:  # noqa: BLE001
+        return None
+    return None
+
+
 def nccl_log_to_stderr():
     """NCCL's INIT lines (version, nRanks, transports) go to stderr, where the driver's log
     capture sees them; stdout stays one JSON line."""
@@ -301,6 +330,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    numa_cores = pin_to_gpu_numa_node(local) if world > 1 else None
     if world > 1:
         nccl_log_to_stderr()
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -428,7 +458,8 @@ def main():
             dist.all_reduce(dts, op=dist.ReduceOp.MAX)
         e2e = {"value": batch * ksteps * world / float(dts.item()), "unit": "img/s",
                "h2d_bytes_per_step": int(x_host.numel() * 4), "d2h_bytes_per_step": int(out_numel * es),
-               "steps": ksteps, "note": "hapi_prefix_forward_host: pinned H2D + forward + D2H, 2-stream pipelined"}
+               "steps": ksteps, "note": "hapi_prefix_forward_host: pinned H2D + forward + D2H, 2-stream pipelined",
+               "host_cores": (f"{len(numa_cores)} cores of the GPU's NUMA node" if numa_cores else "unpinned")}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -98,6 +98,8 @@ struct Geo {
   int cps;                     // K chunks per pipeline stage (modes 3/4: 2 when BN <= 128)
   int pro_c;                   // mode 7: channels of the smem scale/shift tables (C rounded to 64)
   int ph, pw, pq, strips, n_tasks;  // mode 8: pooled map, pool columns per strip, strips/image, tasks
+  int nseg, seg_rows, tlen;         // mode 8: pooled-row segments per (image, strip pair), rows per
+                                    // segment, tiles per task (= seg_rows + 1: a warm-up tile first)
   int ring_bytes;                   // mode 8: two [2 we x 128 B] buffers of vertically pooled rows
   int res_depth;                    // residual ring depth (blocks of [128 x SB] in flight)
   int mt;                           // M sub-tiles per tile sharing each B stage (mode 6: 1 or 2)
@@ -136,8 +138,8 @@ __device__ __forceinline__ long long row_to_m(const ConvArgs& a, const Geo& g, i
 // CTA walks one task's pooled rows in order (the previous stem row stays in registers).
 __device__ __forceinline__ int tile_at(const Geo& g, int k, int num_tiles) {
   if (g.mode == 8) {
-    const int task = blockIdx.x + (k / g.ph) * gridDim.x;
-    return task < g.n_tasks ? task * g.ph + (k - (k / g.ph) * g.ph) : -1;
+    const int task = blockIdx.x + (k / g.tlen) * gridDim.x;
+    return task < g.n_tasks ? task * g.tlen + (k - (k / g.tlen) * g.tlen) : -1;
   }
   if (g.mc) {
     // the two CTAs of a cluster walk the same (M-tile pair, N tile) items in lockstep, rank r
@@ -153,11 +155,13 @@ __device__ __forceinline__ int tile_at(const Geo& g, int k, int num_tiles) {
 
 // Spatial origin of m-tile tm in mode 4 (output coordinates).
 __device__ __forceinline__ void tile_origin(const Geo& g, int tm, int* w0, int* h0, int* b0) {
-  if (g.mode == 8) {  // (image, strip pair, pooled row): strip coordinate 2p, s2d rows from 2po
-    const int po = tm % g.ph, task = tm / g.ph;
-    *b0 = task / g.strips;            // g.strips = strip pairs per image in mode 8
-    *w0 = 2 * (task % g.strips);
-    *h0 = 2 * po;
+  if (g.mode == 8) {  // (image, strip pair, segment, tile): strip coordinate 2p, s2d rows from 2po
+    const int t = tm % g.tlen, task = tm / g.tlen;
+    const int seg = task % g.nseg, pt = task / g.nseg;
+    const int po = seg * g.seg_rows - 1 + t;  // t = 0: the warm-up tile (pooled row before the segment)
+    *b0 = pt / g.strips;              // g.strips = strip pairs per image in mode 8
+    *w0 = 2 * (pt % g.strips);
+    *h0 = 2 * po;                     // -2 for the first segment: TMA zero fill
     return;
   }
   const int tw = tm % g.tiles_w, th = (tm / g.tiles_w) % g.tiles_h, tb = tm / (g.tiles_w * g.tiles_h);
@@ -365,31 +369,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       qcol[n_items] = k * g.pq + qo;
       cgo[n_items] = cg * 8;
     }
-    int po = 0, task = blockIdx.x;
+    int t = 0, task = blockIdx.x;
     for (int it = 0; task < g.n_tasks; ++it) {
-      const int img = task / g.strips, pair = task - img * g.strips;
+      const int pt = task / g.nseg, seg = task - pt * g.nseg;
+      const int img = pt / g.strips, pair = pt - img * g.strips;
+      const int po = seg * g.seg_rows - 1 + t;
       mbar_wait(&pready[it & 1], (it >> 1) & 1);
-      const uint32_t vbuf = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2));
-      __nv_bfloat16* yrow = yb + (((long long)img * g.ph + po) * g.pw + 2 * pair * g.pq) * a.y_ld;
-      const int qlim = g.pw - 2 * pair * g.pq;
+      if (t > 0 && po < g.ph) {  // the warm-up tile only seeds the vertical pool; rows past ph are dead
+        const uint32_t vbuf = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2));
+        __nv_bfloat16* yrow = yb + (((long long)img * g.ph + po) * g.pw + 2 * pair * g.pq) * a.y_ld;
+        const int qlim = g.pw - 2 * pair * g.pq;
 #pragma unroll
-      for (int i = 0; i < M8_MAX_ITEMS; ++i) {
-        if (i >= n_items || qcol[i] >= qlim) continue;
-        uint32_t mx[4] = {0u, 0u, 0u, 0u};
+        for (int i = 0; i < M8_MAX_ITEMS; ++i) {
+          if (i >= n_items || qcol[i] >= qlim) continue;
+          uint32_t mx[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int dc = 0; dc < 3; ++dc) {
-          uint32_t u[4];
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
-                       : "r"(vbuf + off[i][dc]));
+          for (int dc = 0; dc < 3; ++dc) {
+            uint32_t u[4];
+            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
+                         : "r"(vbuf + off[i][dc]));
 #pragma unroll
-          for (int j = 0; j < 4; ++j) mx[j] = bf16x2_max(mx[j], u[j]);
+            for (int j = 0; j < 4; ++j) mx[j] = bf16x2_max(mx[j], u[j]);
+          }
+          *reinterpret_cast<uint4*>(yrow + (long long)qcol[i] * a.y_ld + cgo[i]) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
         }
-        *reinterpret_cast<uint4*>(yrow + (long long)qcol[i] * a.y_ld + cgo[i]) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
       }
       mbar_arrive(&pfree[it & 1]);
-      if (++po == g.ph) {
-        po = 0;
+      if (++t == g.tlen) {
+        t = 0;
         task += gridDim.x;
       }
     }
@@ -412,17 +420,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       bias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
       prev[j] = 0.f;
     }
-    int po = 0, task = blockIdx.x;
+    // a task = (image, strip pair, segment of seg_rows pooled rows); its first tile is the
+    // pooled row before the segment (stem rows -2, -1 -- all padding -- for the first segment),
+    // whose only use is to leave relu(stem row 2 h0 - 1) in prev for the segment's first row
+    int t = 0, task = blockIdx.x;
     float bv0[32], bv1[32];  // bias, or -inf where the stem position is padding (max ignores it)
     for (int it = 0; task < g.n_tasks; ++it) {
       const int acc = it & 1;
-      const int pair = task % g.strips;
+      const int pt = task / g.nseg;
+      const int pair = pt % g.strips;
+      const int po = (task - pt * g.nseg) * g.seg_rows - 1 + t;
       const int stem_col = 2 * (2 * pair + k) * g.pq - 1 + x;
       const bool valid = live && stem_col >= 0 && stem_col < a.OW;
-      const bool valid1 = valid && 2 * po + 1 < a.OH;
+      const bool valid0 = valid && 2 * po >= 0 && 2 * po < a.OH;
+      const bool valid1 = valid && 2 * po + 1 >= 0 && 2 * po + 1 < a.OH;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        bv0[j] = valid ? bias[j] : -INFINITY;
+        bv0[j] = valid0 ? bias[j] : -INFINITY;
         bv1[j] = valid1 ? bias[j] : -INFINITY;
       }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
@@ -461,11 +475,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       fence_proxy_async_smem();
       mbar_arrive(&pready[it & 1]);
-      if (++po == g.ph) {
-        po = 0;
+      if (++t == g.tlen) {
+        t = 0;
         task += gridDim.x;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) prev[j] = 0.f;  // a new (image, strip pair): row -1 is padding
       }
     }
   } else if (warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
@@ -1421,11 +1433,25 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     const int S = (g.pw + 29) / 30;
     g.pq = (g.pw + S - 1) / S;
     g.strips = (S + 1) / 2;                    // strip pairs
-    g.n_tasks = a.N * g.strips;
+    // pooled rows split into nseg segments per (image, strip pair) so the task count fills the
+    // last wave (b512 at 224: 512 tasks = 3.46 waves -> 1024 = 6.92); each segment pays one
+    // warm-up tile.  Pick the split with the shortest makespan, waves x (seg_rows + 1)
+    {
+      const int pairs = a.N * g.strips;
+      long long best = -1;
+      for (int ns = 1; ns <= 8 && ns <= g.ph; ++ns) {
+        const int rows = (g.ph + ns - 1) / ns;
+        const long long waves = ((long long)pairs * ns + num_sms - 1) / num_sms;
+        const long long span = waves * (rows + 1);
+        if (best < 0 || span < best) { best = span; g.nseg = ns; g.seg_rows = rows; }
+      }
+      g.tlen = g.seg_rows + 1;
+      g.n_tasks = pairs * g.nseg;
+    }
     g.we = 2 * g.pq + 4;
     g.wb = 2 * g.pq + 1; g.hb = 2; g.nb = 1;
     g.tiles_w = 1; g.tiles_h = 1;
-    g.m_tiles = g.n_tasks * g.ph;
+    g.m_tiles = g.n_tasks * g.tlen;
     g.cblocks = 1;
     g.k_chunks = 5;                            // resident weights: 5 x 16 KB = 20 chunks x 4 KB
     g.a_bytes = 2 * (16 * g.we * 2 * M8_ROWS); // two planes of [5 rows][2 strips][we] x 16 B
