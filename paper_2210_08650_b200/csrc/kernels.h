@@ -166,6 +166,10 @@ struct PoolArgs {
   const void* x; int N, H, W, C, x_ld;
   void* y; int OH, OW, y_ld;
   int k, stride, pad, mode;
+  // optional bn-relu prologue: x := relu(x * pro_scale[c] + pro_shift[c]) before pooling (the
+  // DenseNet transition commuted to bn-relu -> avgpool -> 1x1 conv, model.cu)
+  const float* pro_scale = nullptr;
+  const float* pro_shift = nullptr;
 };
 cudaError_t pool_launch(const PoolArgs& a, int is_bf16, cudaStream_t st);
 

@@ -214,6 +214,10 @@ __global__ void pool_kernel(const PoolArgs a) {
         if ((unsigned)iw >= (unsigned)a.W) continue;
         float f[V];
         load_vec<T, V>(x + ((n * a.H + ih) * a.W + iw) * a.x_ld + c, f);
+        if (a.pro_scale) {
+#pragma unroll
+          for (int j = 0; j < V; ++j) f[j] = fmaxf(fmaf(f[j], __ldg(a.pro_scale + c + j), __ldg(a.pro_shift + c + j)), 0.f);
+        }
 #pragma unroll
         for (int j = 0; j < V; ++j) acc[j] = a.mode == 0 ? fmaxf(acc[j], f[j]) : acc[j] + f[j];
       }
@@ -251,6 +255,17 @@ __global__ void __launch_bounds__(256) pool2x2_bf16_kernel(const PoolArgs a) {
     load_vec<__nv_bfloat16, 8>(p0 + a.x_ld, f[1]);
     load_vec<__nv_bfloat16, 8>(p1, f[2]);
     load_vec<__nv_bfloat16, 8>(p1 + a.x_ld, f[3]);
+    if (a.pro_scale) {  // bn-relu prologue (commuted DenseNet transition)
+      float sc[8], sh[8];
+      load_vec<float, 4>(a.pro_scale + c, *reinterpret_cast<float(*)[4]>(sc));
+      load_vec<float, 4>(a.pro_scale + c + 4, *reinterpret_cast<float(*)[4]>(sc + 4));
+      load_vec<float, 4>(a.pro_shift + c, *reinterpret_cast<float(*)[4]>(sh));
+      load_vec<float, 4>(a.pro_shift + c + 4, *reinterpret_cast<float(*)[4]>(sh + 4));
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[t][j] = fmaxf(fmaf(f[t][j], sc[j], sh[j]), 0.f);
+    }
     float acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {

@@ -151,6 +151,14 @@ bool halo_enabled() {
   return on;
 }
 
+bool commute_enabled() {  // HAPI_COMMUTE=0: DenseNet transitions as bn-relu-conv, then avgpool
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_COMMUTE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool fused_ds_disabled() {
   static const bool off = [] {
     const char* e = std::getenv("HAPI_FUSE_DS");
@@ -861,7 +869,41 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         break;
       }
       case MK_BN: {
-        if (i + 2 < split && mods[i + 1].kind == MK_RELU && mods[i + 2].kind == MK_CONV) {
+        if (i + 3 < split && mods[i + 1].kind == MK_RELU && mods[i + 2].kind == MK_CONV && mods[i + 2].k == 1 &&
+            mods[i + 2].stride == 1 && mods[i + 2].pad == 0 && !mods[i + 2].bias && mods[i + 3].kind == MK_AVGPOOL &&
+            mods[i + 3].k == 2 && mods[i + 3].stride == 2 && mods[i + 3].pad == 0 && cur.H % 2 == 0 &&
+            cur.W % 2 == 0 && commute_enabled()) {
+          // DenseNet transition with its pool inside the prefix: avgpool2x2(conv1x1(relu(bn x)))
+          // = conv1x1(avgpool2x2(relu(bn x))) (a bias-free 1x1 conv and a 2x2 mean are both
+          // linear and act on different axes), so pool first -- the conv then runs on a quarter
+          // of the pixels and the C/2-channel full-size map never reaches HBM
+          const ModDesc& cv = mods[i + 2];
+          float *dsc, *dsh;
+          auto it = m->bn_cache.find(md.name);
+          if (it != m->bn_cache.end()) {
+            dsc = it->second.first;
+            dsh = it->second.second;
+          } else {
+            std::vector<double> sc, sh;
+            if (!bn_affine(m, md.name, md.cin, sc, sh)) return set_error(HAPI_ERR_INVALID_MODEL, "bn %s", md.name.c_str());
+            std::vector<float> fsc(sc.begin(), sc.end()), fsh(sh.begin(), sh.end());
+            if ((st = upload(m, fsc, &dsc)) != HAPI_OK || (st = upload(m, fsh, &dsh)) != HAPI_OK) return st;
+            m->bn_cache[md.name] = {dsc, dsh};
+          }
+          View pooled = b.compact(cur.C, cur.H / 2, cur.W / 2);
+          b.pool(cur, pooled, 2, 2, 0, 1);
+          b.p.ops.back().scale = dsc;
+          b.p.ops.back().shift = dsh;
+          b.p.ops.back().desc = "bn-relu + avgpool 2x2/s2 (transition commuted) C" + std::to_string(cur.C);
+          ConvSpec cs;
+          cs.wname = cv.name + ".weight";
+          cs.cin = cv.cin; cs.cout = cv.cout; cs.k = 1; cs.stride = 1; cs.pad = 0;
+          cs.cs = pooled.C;
+          View o = b.compact(cv.cout, pooled.H, pooled.W);
+          if ((st = b.conv(cs, pooled, o, false, nullptr)) != HAPI_OK) return st;
+          cur = o;
+          i += 4;
+        } else if (i + 2 < split && mods[i + 1].kind == MK_RELU && mods[i + 2].kind == MK_CONV) {
           // DenseNet transition norm -> relu -> conv: bn-relu prologue on the conv's A operand
           const ModDesc& cv = mods[i + 2];
           ConvSpec cs;
@@ -1351,6 +1393,8 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.y = vptr(m, p, o.out, out);
       a.OH = o.out.H; a.OW = o.out.W; a.y_ld = o.out.buf < 0 ? o.out.C : o.out.ld;
       a.k = o.pk; a.stride = o.ps; a.pad = o.pp; a.mode = o.pmode;
+      a.pro_scale = o.scale;
+      a.pro_shift = o.shift;
       e = pool_launch(a, isb, st);
       break;
     }

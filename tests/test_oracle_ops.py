@@ -137,3 +137,23 @@ def test_linear_brute():
 def test_relu():
     x = np.array([-1.0, 0.0, 2.5, -0.0])
     np.testing.assert_array_equal(ops.relu(x), [0.0, 0.0, 2.5, 0.0])
+
+
+def test_transition_pool_commutes_with_bias_free_1x1_conv():
+    """The identity the executor's commuted DenseNet transition relies on (SURVEY
+    K5): for a bias-free 1x1 conv W and the 2x2/s2 mean, avgpool(conv(y)) = conv(avgpool(y))
+    for any y = relu(bn(x)) -- checked on the oracle's own operators, where it holds to
+    rounding."""
+    import numpy as np
+    from oracle import ops
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((2, 12, 8, 6))
+    g, b, m, v = rng.uniform(0.8, 1.2, 12), rng.uniform(-.1, .1, 12), rng.uniform(-.1, .1, 12), rng.uniform(.8, 1.2, 12)
+    w = rng.standard_normal((5, 12, 1, 1))
+    y = ops.relu(ops.batchnorm_eval(x, g, b, m, v))
+    a = ops.avgpool2d(ops.conv2d(y, w, None, 1, 0), 2, 2)
+    c = ops.conv2d(ops.avgpool2d(y, 2, 2), w, None, 1, 0)
+    np.testing.assert_allclose(a, c, rtol=1e-12, atol=1e-12)
+    # and it fails with a bias-carrying or non-1x1 conv (why the planner checks both)
+    k3 = rng.standard_normal((5, 12, 3, 3))
+    assert not np.allclose(ops.avgpool2d(ops.conv2d(y, k3, None, 1, 1), 2, 2), ops.conv2d(ops.avgpool2d(y, 2, 2), k3, None, 1, 1))
