@@ -424,7 +424,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // pooled row before the segment (stem rows -2, -1 -- all padding -- for the first segment),
     // whose only use is to leave relu(stem row 2 h0 - 1) in prev for the segment's first row
     int t = 0, task = blockIdx.x;
-    float bv0[32], bv1[32];  // bias, or -inf where the stem position is padding (max ignores it)
     for (int it = 0; task < g.n_tasks; ++it) {
       const int acc = it & 1;
       const int pt = task / g.nseg;
@@ -432,13 +431,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int po = (task - pt * g.nseg) * g.seg_rows - 1 + t;
       const int stem_col = 2 * (2 * pair + k) * g.pq - 1 + x;
       const bool valid = live && stem_col >= 0 && stem_col < a.OW;
-      const bool valid0 = valid && 2 * po >= 0 && 2 * po < a.OH;
+      const bool valid0 = valid && 2 * po >= 0 && 2 * po < a.OH;  // padding positions are -inf
       const bool valid1 = valid && 2 * po + 1 >= 0 && 2 * po + 1 < a.OH;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        bv0[j] = valid0 ? bias[j] : -INFINITY;
-        bv1[j] = valid1 ? bias[j] : -INFINITY;
-      }
       mbar_wait(&tfull[acc], (it >> 1) & 1);
       tc_fence_after();
       uint32_t v0[32], v1[32];
@@ -461,8 +455,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int h = 0; h < 2; ++h) {
               // prev >= 0, so max(prev, a, b) = max(prev, relu(a), relu(b)); padding is -inf
               const int c = c4 * 8 + 2 * j + h;
-              const float a0 = __uint_as_float(v0[c]) + bv0[c];
-              const float a1 = __uint_as_float(v1[c]) + bv1[c];
+              const float a0 = valid0 ? __uint_as_float(v0[c]) + bias[c] : -INFINITY;
+              const float a1 = valid1 ? __uint_as_float(v1[c]) + bias[c] : -INFINITY;
               f[h] = fmaxf(fmaxf(prev[c], a0), a1);
               prev[c] = fmaxf(a1, 0.f);
             }
@@ -1439,7 +1433,11 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     {
       const int pairs = a.N * g.strips;
       long long best = -1;
-      for (int ns = 1; ns <= 8 && ns <= g.ph; ++ns) {
+      static const int max_seg = [] {  // HAPI_STEM_SEG=0: one task per (image, strip pair)
+        const char* e = std::getenv("HAPI_STEM_SEG");
+        return (e && e[0] == '0') ? 1 : 8;
+      }();
+      for (int ns = 1; ns <= max_seg && ns <= g.ph; ++ns) {
         const int rows = (g.ph + ns - 1) / ns;
         const long long waves = ((long long)pairs * ns + num_sms - 1) / num_sms;
         const long long span = waves * (rows + 1);

@@ -6,6 +6,10 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 
+#ifndef HAPI_WATCHDOG_NS
+#define HAPI_WATCHDOG_NS 20000000000ull
+#endif
+
 namespace hapi {
 namespace tcx {
 
@@ -29,12 +33,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t spins = 0;
   uint64_t t0 = 0;
   while (!done) {
-    // watchdog: a lost arrival must fail loudly (trap after ~2 s) instead of hanging the GPU
+    // watchdog: a lost arrival must fail loudly (trap after HAPI_WATCHDOG_NS, 20 s: long
+    // enough for kernels slowed down by compute-sanitizer) instead of hanging the GPU
     if ((++spins & 1023u) == 0) {
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (t0 == 0) t0 = now;
-      else if (now - t0 > 2000000000ull) __trap();
+      else if (now - t0 > HAPI_WATCHDOG_NS) __trap();
     }
     asm volatile(
         "{\n\t.reg .pred p;\n\t"

@@ -78,7 +78,7 @@ def test_suffix_argument_errors():
         m.forward(6, x, out)                                                      # prefix entry on a suffix model
     acts = torch.zeros(2 * m.out_bytes[3] // 2, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(H.HapiError):
-        m.forward_suffix(9, acts, out)                                            # end outside [6, 8]
+        m.forward_suffix(9, acts.view(2, -1), out)                                            # end outside [6, 8]
     with pytest.raises(ValueError):
         m.forward_suffix(7, out, out)                                             # acts not 2 layer-4 outputs
     m.close()
