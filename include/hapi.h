@@ -284,6 +284,16 @@ HAPI_API hapi_status hapi_suffix_forward(hapi_model *m, uint32_t end_idx, const 
 HAPI_API hapi_status hapi_prefix_forward_host(hapi_model *m, uint32_t split_idx, const float *images,
                                      uint64_t batch, void *out);
 
+/* The same, enqueued without waiting: returns once the copies and launches are queued.
+ * Calls may follow each other back to back -- the staging slots alternate across calls, so
+ * the H2D of the next call overlaps the compute of the previous one (a stream of requests
+ * pays the pipeline fill and drain once).  `images` must stay valid and `out` unread until
+ * hapi_host_sync(m) returns.  Errors as hapi_prefix_forward_host. */
+HAPI_API hapi_status hapi_prefix_forward_host_async(hapi_model *m, uint32_t split_idx, const float *images,
+                                                   uint64_t batch, void *out);
+/* Wait for every host-path call enqueued on the model (its copy streams and its stream). */
+HAPI_API hapi_status hapi_host_sync(hapi_model *m);
+
 /* Device bytes owned by the model: packed weights (+bias/BN vectors), and the activation
  * arena plus the host-path staging (desc.host_chunk) in *arena_bytes. */
 HAPI_API hapi_status hapi_model_device_bytes(const hapi_model *m, uint64_t *weight_bytes, uint64_t *arena_bytes);

@@ -338,6 +338,18 @@ class Model:
         _check(_lib.hapi_prefix_forward_host(self._h, split_idx, C.c_void_p(ip), images.shape[0], C.c_void_p(op)))
         return out
 
+    def forward_host_async(self, split_idx: int, images, out):
+        """Enqueue a host-buffer call without waiting (hapi_prefix_forward_host_async): keep
+        `images` and `out` alive and untouched until host_sync()."""
+        self._check_images(images, False)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), False)
+        _check(_lib.hapi_prefix_forward_host_async(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
+                                                   C.c_void_p(out.data_ptr())))
+        return out
+
+    def host_sync(self):
+        _check(_lib.hapi_host_sync(self._h))
+
     def forward_timed(self, split_idx: int, images, out) -> List[float]:
         self._check_images(images, True)
         self._check_out(out, images.shape[0] * self._split_bytes(split_idx), True)

@@ -62,6 +62,9 @@ hapi_model_create_shared = _sig("hapi_model_create_shared", C.c_int, C.c_void_p,
 hapi_model_set_stream = _sig("hapi_model_set_stream", C.c_int, C.c_void_p, C.c_void_p)
 hapi_prefix_forward = _sig("hapi_prefix_forward", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
 hapi_prefix_forward_host = _sig("hapi_prefix_forward_host", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
+hapi_prefix_forward_host_async = _sig("hapi_prefix_forward_host_async", C.c_int, C.c_void_p, u32, C.c_void_p, u64,
+                                      C.c_void_p)
+hapi_host_sync = _sig("hapi_host_sync", C.c_int, C.c_void_p)
 hapi_model_device_bytes = _sig("hapi_model_device_bytes", C.c_int, C.c_void_p, P_u64, P_u64)
 hapi_plan_info = _sig("hapi_plan_info", C.c_int, C.c_void_p, u32, P_u32, P_u32, P_dbl, P_dbl, u32)
 hapi_prefix_forward_timed = _sig("hapi_prefix_forward_timed", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p,
@@ -100,4 +103,5 @@ EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_ch
             "hapi_model_destroy", "hapi_last_error", "hapi_build_info", "hapi_scheduler_create",
             "hapi_scheduler_submit", "hapi_scheduler_poll", "hapi_scheduler_finish", "hapi_scheduler_query",
             "hapi_scheduler_destroy", "hapi_model_create_shared", "hapi_server_create", "hapi_server_add_model",
-            "hapi_server_submit", "hapi_server_step", "hapi_server_query", "hapi_server_destroy"]
+            "hapi_server_submit", "hapi_server_step", "hapi_server_query", "hapi_server_destroy",
+            "hapi_prefix_forward_host_async", "hapi_host_sync"]

@@ -296,6 +296,7 @@ struct hapi_model {
   int64_t stage_out_bytes = 0;
   cudaEvent_t ev[8] = {};
   bool host_ready = false;
+  uint64_t host_seq = 0;                // host-path chunks enqueued so far (slot parity, reuse waits)
   // CUDA graphs of one chunk's launch sequence, keyed by (split, batch, images, out)
   struct GraphEntry {
     uint32_t split;
@@ -1914,7 +1915,33 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
   return st;
 }
 
+static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
+                                        void* out);
+
 hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
+  hapi_status st = forward_host_enqueue(m, split_idx, images, batch, out);
+  if (st != HAPI_OK) return st;
+  return hapi_host_sync(m);
+}
+
+hapi_status hapi_prefix_forward_host_async(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
+                                           void* out) {
+  return forward_host_enqueue(m, split_idx, images, batch, out);
+}
+
+hapi_status hapi_host_sync(hapi_model* m) {
+  clear_error();
+  if (!m) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null model");
+  if (!m->host_ready) return HAPI_OK;
+  DeviceGuard dg(m->d.device);
+  HAPI_CUDA_TRY(cudaStreamSynchronize(m->copy_stream));
+  HAPI_CUDA_TRY(cudaStreamSynchronize(m->out_stream));
+  HAPI_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  return HAPI_OK;
+}
+
+static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
+                                        void* out) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
@@ -1952,15 +1979,19 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
   }
   const uint64_t nchunks = sizes.size();
   uint64_t c0 = 0;
+  // chunk numbering continues across calls (host_seq), so consecutive asynchronous calls keep
+  // alternating the two staging slots and wait on the chunk that last used a slot -- the H2D of
+  // the next call's first chunk overlaps the compute of this call's last one
   for (uint64_t c = 0; c < nchunks; c0 += sizes[c], ++c) {
-    const int k = (int)(c & 1);
+    const uint64_t gc = m->host_seq++;
+    const int k = (int)(gc & 1);
     const int nb = (int)sizes[c];
-    if (c >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(xs, m->ev[2 + k], 0));  // stage_in[k] free once chunk c-2 computed
+    if (gc >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(xs, m->ev[2 + k], 0));  // stage_in[k] free once chunk gc-2 computed
     HAPI_CUDA_TRY(cudaMemcpyAsync(m->stage_in[k], reinterpret_cast<const char*>(images) + c0 * img_bytes,
                                   (size_t)nb * img_bytes, cudaMemcpyHostToDevice, xs));
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[k], xs));
     HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[k], 0));
-    if (c >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[4 + k], 0));  // stage_out[k] drained
+    if (gc >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[4 + k], 0));  // stage_out[k] drained
     hapi_status st = run_chunk_graph(m, *p, nb, static_cast<const float*>(m->stage_in[k]), m->stage_out[k]);
     if (st != HAPI_OK) return st;
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[2 + k], cs));
@@ -1969,9 +2000,6 @@ hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const fl
                                   (size_t)nb * p->out_bytes_per_img, cudaMemcpyDeviceToHost, ys));
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[4 + k], ys));
   }
-  HAPI_CUDA_TRY(cudaStreamSynchronize(xs));
-  HAPI_CUDA_TRY(cudaStreamSynchronize(ys));
-  HAPI_CUDA_TRY(cudaStreamSynchronize(cs));
   return HAPI_OK;
 }
 

@@ -262,3 +262,28 @@ def test_gpu_argument_errors():
         assert e.value.status == 1
     with pytest.raises(H.HapiError):
         m.forward(13, x[:0], out)
+
+
+def test_host_async_stream_matches_sync_and_oracle():
+    """hapi_prefix_forward_host_async: back-to-back calls share the staging slots (chunk
+    numbering continues across calls) -- every call's output equals the synchronous call's,
+    bitwise, and the oracle on sampled images."""
+    import torch
+    H = _H()
+    arch, s = "resnet18", 10
+    P = hapi_inputs.params(arch, 12)
+    m = H.Model(arch, "bf16", list(P.values()), 64, s, s, in_h=64, in_w=64, host_chunk=40)
+    xs = [torch.from_numpy(hapi_inputs.images(n, 13 + n, 64, 64)) for n in (100, 37, 64, 5)]
+    outs = [torch.empty(x.shape[0] * m.out_bytes[s - 1] // 2, dtype=torch.bfloat16) for x in xs]
+    for x, o in zip(xs, outs):
+        m.forward_host_async(s, x, o)
+    m.host_sync()
+    for x, o in zip(xs, outs):
+        ref_sync = torch.empty_like(o)
+        m.forward_host(s, x, ref_sync)
+        assert torch.equal(o.view(torch.int16), ref_sync.view(torch.int16))
+        n = x.shape[0]
+        sel = [0, n - 1]
+        ref = oracle_all(arch, 12, 13 + n, n, 64, 64, upto=s, sel=sel)[s - 1]
+        check_close(o.float().numpy().reshape(n, -1)[sel], ref, "bf16", f"host async n={n}")
+    m.close()
