@@ -191,6 +191,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool HALO = (MODE == 6 || MODE == 9);
   constexpr bool IM2COL = (MODE == 5 || MODE == 10);
   constexpr int MT = (MODE == 9 || MODE == 10) ? 2 : 1;
+  // TMEM accumulator buffers: two (the epilogue of tile i overlaps the MMAs of tile i+1) unless
+  // MT x BN x 2 exceeds the 512 columns -- MODE 10 at BN = 256 keeps one buffer of 2 x 256 columns
+  // (the weight stream halves; the MMAs wait for each tile pair's drain)
+  constexpr int NACC = (MT * BN * 2 <= 512) ? 2 : 1;
+  constexpr int TMEM_ALLOC = NACC == 2 ? C::TMEM_COLS * MT : BN * MT;
   constexpr bool TMA_A = (MODE == 3 || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   // 1x1 TMA tiles (mode 3): the epilogue stores per-warp [32 x 32] boxes through the 7th map
@@ -261,7 +266,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(C::TMEM_COLS * MT)
+                 "r"(TMEM_ALLOC)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -583,6 +588,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
           }
           int cb = 0, r = 0, sft = 0;  // (tap, channel block) of chunk kc, tracked incrementally
+#pragma unroll 1
           for (int kc = 0; kc < g.k_chunks; kc += CPS) {
             const int nch = g.k_chunks - kc < CPS ? g.k_chunks - kc : CPS;
             mbar_wait(&empty[stage], phase ^ 1);
@@ -750,8 +756,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (TMA_A && g.b_res) mbar_wait(bres, 0);
       int iter = 0;
       for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
-        const int acc = iter & 1;
-        const uint32_t acc_phase = (iter >> 1) & 1;
+        const int acc = NACC == 2 ? (iter & 1) : 0;
+        const uint32_t acc_phase = NACC == 2 ? ((iter >> 1) & 1) : (iter & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * MT * BN;
@@ -865,6 +871,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           __syncwarp();
           continue;
         }
+#pragma unroll 1
         for (int kc = 0; kc < g.k_chunks; kc += CPS) {
           const int nch = g.k_chunks - kc < CPS ? g.k_chunks - kc : CPS;
           mbar_wait(&full[stage], phase);
@@ -1008,8 +1015,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int k_ = 0, tile = (iter < 0 ? -1 : tile_at(g, 0, num_tiles)); tile >= 0;
          tile = tile_at(g, ++k_, num_tiles), ++iter) {
       const int tn = tile - (tile / g.n_tiles) * g.n_tiles;
-      const int acc = iter & 1;
-      const uint32_t acc_phase = (iter >> 1) & 1;
+      const int acc = NACC == 2 ? (iter & 1) : 0;
+      const uint32_t acc_phase = NACC == 2 ? ((iter >> 1) & 1) : (iter & 1);
       // bias of this tile's columns -> smem, only when the N tile changes (a global load per
       // tile would put an L2 round trip on every tile of the epilogue-bound small-K convs;
       // the previous tile's readers are past the last epi_bar of that tile)
@@ -1223,7 +1230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (g.mc) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::TMEM_COLS * MT)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_ALLOC)
                  : "memory");
   }
 }
@@ -1357,7 +1364,7 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
     case 5:
       if (g.mt == 2) {
-        if constexpr (BN <= 128) return launch_t<BN, 10>(a, g, mp, num_sms, st);
+        if constexpr (BN <= 128 || BN == 256) return launch_t<BN, 10>(a, g, mp, num_sms, st);
         return cudaErrorInvalidValue;
       }
       return launch_t<BN, 5>(a, g, mp, num_sms, st);
@@ -1376,6 +1383,14 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
 }
 
 }  // namespace
+
+bool dual_m256_enabled() {  // HAPI_DUAL_M256=0: im2col convs at BN = 256 with one M tile per weight chunk
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M256");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 bool dual_m_enabled() {
   static const bool on = [] {
@@ -1515,6 +1530,11 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   // im2col convs at BN = 128: two M sub-tiles share every weight chunk (halves the L2 weight
   // stream; TMEM 2 x 2 x 128 columns)
   if (mode == 5 && bn == 128 && g.n_tiles == 1 && !a.res && a.k2_chunks == 0 && dual_m_enabled()) g.mt = 2;
+  // ... and at BN = 256 (one accumulator buffer of 2 x 256 columns): the 3x3 convs of ResNet-50
+  // stage 3 move 1.38 GB through L2 per launch at BN = 256 x 1 M tile (the weights re-read per
+  // 128-pixel tile are two thirds of it); two M tiles per weight chunk cut that to ~0.9 GB
+  if (mode == 5 && bn == 256 && g.n_tiles == 1 && !a.res && a.k2_chunks == 0 && dual_m_enabled() && dual_m256_enabled())
+    g.mt = 2;
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {
     if ((mode != 3 && mode != 4 && mode != 5) || !mp.a2 || (a.k2_diag && (!mp.b2 || bn > 256))) return cudaErrorInvalidValue;

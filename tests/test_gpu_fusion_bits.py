@@ -47,6 +47,8 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("resnet50", 21, 96, 6, "HAPI_STEM_POOL", None, "0"),   # stem conv + maxpool fusion
     ("densenet121", 9, 64, 5, "HAPI_STEM_POOL", None, "0"),
     ("resnet50", 21, 96, 6, "HAPI_DUAL_M", None, "0"),      # two M sub-tiles per weight stage (halo mode)
+    ("resnet50", 21, 224, 3, "HAPI_DUAL_M256", None, "0"),  # ... im2col at BN = 256 (one TMEM buffer), stage 3/4
+    ("resnet50", 21, 160, 3, "HAPI_DUAL_M256", None, "0"),  # ... odd M-tile count
     ("resnet50", 21, 96, 6, "HAPI_CLUSTER", "1", None),     # 2-CTA multicast weights (opt-in)
     ("resnet50", 21, 160, 3, "HAPI_CLUSTER", "1", None),    # ... odd M-tile count (OOB pair tile)
     ("resnet50", 21, 96, 6, "HAPI_SUB_STORE", None, "0"),   # pair output stored at stride 2 for the ds
@@ -96,3 +98,33 @@ def test_vgg_window_stem_matches_gather_stem(tmp_path):
     a, b = fused.astype(np.float64).ravel(), plain.astype(np.float64).ravel()
     assert np.linalg.norm(a - b) <= 4e-3 * np.linalg.norm(b)
 
+
+
+_ORACLE_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import hapi_inputs
+from tests.gpu_helpers import gpu_forward, oracle_all
+from tests.parity_check import check_close
+arch, n, size = "densenet121", 3, 64
+P = hapi_inputs.params(arch, 11)
+x = hapi_inputs.images(n, 12, size, size)
+for s in (9, 14, 19, 20, 22):
+    y, m = gpu_forward(arch, "bf16", s, x, P)
+    m.close()
+    check_close(y, oracle_all(arch, 11, 12, n, size, size, upto=s)[s - 1], "bf16", "commute %s s=%d" % ({flag!r}, s))
+print("ok")
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("flag", ["1", "0"])
+def test_transition_commute_both_ways_match_oracle(flag):
+    """DenseNet transitions with the avgpool moved ahead of the 1x1 conv (default) and in the
+    paper's order (HAPI_COMMUTE=0): both within the parity bounds at splits after each
+    transition (not bitwise: the pooled intermediate is rounded to bf16 before the conv)."""
+    env = dict(os.environ)
+    env["HAPI_COMMUTE"] = flag
+    r = subprocess.run([sys.executable, "-c", _ORACLE_SNIPPET.format(root=ROOT, flag=flag)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
