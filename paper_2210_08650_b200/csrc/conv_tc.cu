@@ -190,19 +190,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // MODE 10 = im2col mode 5 with two M sub-tiles per weight stage
   constexpr bool HALO = (MODE == 6 || MODE == 9);
   constexpr bool IM2COL = (MODE == 5 || MODE == 10);
-  constexpr int MT = (MODE == 9 || MODE == 10) ? 2 : 1;
+  // MODE 11 = 1x1 mode 3 with two M sub-tiles per weight chunk (g.mode stays 3)
+  constexpr int MT = (MODE == 9 || MODE == 10 || MODE == 11) ? 2 : 1;
+  constexpr bool FLAT = (MODE == 3 || MODE == 11);  // 2D [M][C] TMA tiles
   // TMEM accumulator buffers: two (the epilogue of tile i overlaps the MMAs of tile i+1) unless
   // MT x BN x 2 exceeds the 512 columns -- MODE 10 at BN = 256 keeps one buffer of 2 x 256 columns
   // (the weight stream halves; the MMAs wait for each tile pair's drain)
   constexpr int NACC = (MT * BN * 2 <= 512) ? 2 : 1;
   constexpr int TMEM_ALLOC = NACC == 2 ? C::TMEM_COLS * MT : BN * MT;
-  constexpr bool TMA_A = (MODE == 3 || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
+  constexpr bool TMA_A = (FLAT || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   // 1x1 TMA tiles (mode 3): the epilogue stores per-warp [32 x 32] boxes through the 7th map
   // (tmap_bh, free in mode 3: no multicast there); the CTA-wide staging path is compiled only
   // into the other modes.  (Measured: -3..-5% on the epilogue-bound 1x1 convs.  Tried on the
   // im2col modes too: +7..9% on the MMA-bound 3x3 convs, so they keep the staging block.)
-  constexpr bool WARP_STORE = (MODE == 3);
+  constexpr bool WARP_STORE = FLAT;
   const int S = g.stages;
   const int AS = (HALO || MODE == 8) ? g.a_stages : S;
   constexpr int CPS = (MODE == 3 && BN <= 128) ? 2 : 1;  // == g.cps (host); mode 4 measured better at 1
@@ -595,6 +597,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (elect_one()) {
               mbar_arrive_expect_tx(&full[stage], nch * (nsub * g.a_bytes + (g.b_res ? 0 : C::B_STAGE_BYTES)));
               int cb_j = cb, r_j = r, s_j = sft;
+#pragma unroll 1
               for (int j = 0; j < nch; ++j) {
                 const int ck = kc + j;
                 const uint32_t dA = smem_u32(sA + stage * ASZ + j * A_STAGE_BYTES);
@@ -603,14 +606,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   // the identity residual (k2_diag) -- channel block tn*BN + 64 j of the residual
                   // against chunk j of the shared identity (tmap_b2)
                   const int c2 = ck - g.k1_chunks + (a.k2_diag ? tn * (BN / BK) : 0);
-                  if (MODE == 3)
+                  if (FLAT)
                     tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
                   else if (IM2COL)
                     tma_load_im2col_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, 0, 0, &full[stage]);
                   else
                     tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
-                } else if (MODE == 3) {
+                } else if (FLAT) {
                   tma_load_2d(dA, &tmap_a, ck * BK, tm * BM, &full[stage]);
+                  if (MT > 1 && nsub > 1)  // MODE 11: the second M sub-tile of the weight chunk
+                    tma_load_2d(dA + A_STAGE_BYTES, &tmap_a, ck * BK, (tm + 1) * BM, &full[stage]);
                 } else if (IM2COL) {
                   tma_load_im2col_4d(dA, &tmap_a, cb_j * BK, w0, h0, b0, (uint16_t)s_j, (uint16_t)r_j, &full[stage]);
                   if (MT > 1 && nsub > 1)
@@ -637,6 +642,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             __syncwarp();
             if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
+#pragma unroll 1
             for (int j = 0; j < nch; ++j) {
               if (++cb == g.cblocks) {
                 cb = 0;
@@ -877,6 +883,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (elect_one()) {
+#pragma unroll 1
             for (int j = 0; j < nch; ++j) {
               const uint64_t adesc = make_sdesc(sA0 + stage * ASZ + j * A_STAGE_BYTES);
               const uint64_t bdesc =
@@ -1279,7 +1286,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   }
   g.res_box_bytes = (g.mode == 4 || g.mode == 6) ? C::SB * 2 * g.wb * g.hb * g.nb : C::SB_BYTES;
   int smem;
-  g.cps = (g.mode == 3 && BN <= 128) ? 2 : 1;
+  g.cps = (g.mode == 3 && BN <= 128 && g.mt == 1) ? 2 : 1;
   g.res_depth = res_depth_pick(g.cps * C::STAGE_BYTES, C::FIXED, C::SB_BYTES);
   const int res_bytes = g.has_res ? g.res_depth * C::SB_BYTES : 0;
   const int bres_bytes = g.k_chunks * C::B_STAGE_BYTES;
@@ -1336,7 +1343,7 @@ cudaError_t launch_t(const ConvArgs& a, Geo g, const ConvMaps& mp, int num_sms, 
   if (!g.mc)
     return launch_pdl(conv_tc_kernel<BN, MODE>, dim3(grid), dim3(NUM_THREADS), (size_t)smem, st, a, g,
                       mp.a ? *mp.a : *b, *b, mp.y ? *mp.y : *b, mp.r ? *mp.r : *b, mp.a2 ? *mp.a2 : *b,
-                      mp.b2 ? *mp.b2 : *b, (MODE == 3 && mp.yw) ? *mp.yw : *b);
+                      mp.b2 ? *mp.b2 : *b, ((MODE == 3 || MODE == 11) && mp.yw) ? *mp.yw : *b);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(NUM_THREADS);
@@ -1360,7 +1367,12 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
   switch (g.mode) {
     case 0: return launch_t<BN, 0>(a, g, mp, num_sms, st);
     case 2: return launch_t<BN, 2>(a, g, mp, num_sms, st);
-    case 3: return launch_t<BN, 3>(a, g, mp, num_sms, st);
+    case 3:
+      if (g.mt == 2) {
+        if constexpr (BN == 128 || BN == 256) return launch_t<BN, 11>(a, g, mp, num_sms, st);
+        return cudaErrorInvalidValue;
+      }
+      return launch_t<BN, 3>(a, g, mp, num_sms, st);
     case 4: return launch_t<BN, 4>(a, g, mp, num_sms, st);
     case 5:
       if (g.mt == 2) {
@@ -1383,6 +1395,14 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
 }
 
 }  // namespace
+
+bool dual_m1x1_enabled() {  // HAPI_DUAL_M1X1=1: 1x1 convs with two M sub-tiles per weight chunk (MODE 11)
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M1X1");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 bool dual_m256_enabled() {  // HAPI_DUAL_M256=0: im2col convs at BN = 256 with one M tile per weight chunk
   static const bool on = [] {
@@ -1534,6 +1554,13 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   // stage 3 move 1.38 GB through L2 per launch at BN = 256 x 1 M tile (the weights re-read per
   // 128-pixel tile are two thirds of it); two M tiles per weight chunk cut that to ~0.9 GB
   if (mode == 5 && bn == 256 && g.n_tiles == 1 && !a.res && a.k2_chunks == 0 && dual_m_enabled() && dual_m256_enabled())
+    g.mt = 2;
+  // 1x1 convs without a residual (every bottleneck's conv1) likewise: the K = 512..2048 weight
+  // chunks are re-read per 128-row tile otherwise (ResNet-50 stage 3 conv1: 411 of 616 MB through
+  // L2 per launch).  Measured a loss (stage-3 conv1 +8%, layer3.0.conv1 +16%: with one TMEM
+  // buffer the short-K tiles wait for every drain), so opt-in: HAPI_DUAL_M1X1=1 (MODE 11)
+  if (mode == 3 && (bn == 256 || bn == 128) && !a.res && a.k2_chunks == 0 && a.nchw == 0 && dual_m_enabled() &&
+      dual_m1x1_enabled() && (long long)((g.m_tiles + 1) / 2) * g.n_tiles >= 2LL * num_sms)
     g.mt = 2;
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {
