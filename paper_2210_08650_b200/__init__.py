@@ -253,6 +253,8 @@ class Model:
     def shared(self, max_batch: int, host_chunk: int = 0) -> "Model":
         """hapi_model_create_shared: a model over this model's device weights (no copy) with
         its own arena for max_batch images -- one per concurrent request."""
+        if host_chunk < 0:
+            host_chunk = max_batch if max_batch < 256 else min(max_batch, max(64, (max_batch * 3 // 16 + 15) // 16 * 16))
         h = C.c_void_p()
         _check(_lib.hapi_model_create_shared(self._h, max_batch, host_chunk, C.byref(h)))
         m = object.__new__(Model)

@@ -567,6 +567,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int nsub = MT == 1 ? 1 : (g.m_tiles - tm < MT ? g.m_tiles - tm : MT);
           int ow0 = 0, oh0 = 0, b0 = 0, w0 = 0, h0 = 0;
           int w1 = 0, h1 = 0, b1 = 0;  // MODE 10: origin of the second M sub-tile
+          int ow1o = 0, oh1o = 0;      // ... in output coordinates (fused-downsample source)
           if (SPATIAL) {
             tile_origin(g, tm, &ow0, &oh0, &b0);
             w0 = ow0 * a.stride - a.pad;
@@ -587,6 +588,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int oh1 = rem1 / a.OW, ow1 = rem1 - (rem1 / a.OW) * a.OW;
               w1 = ow1 * a.stride - a.pad;
               h1 = oh1 * a.stride - a.pad;
+              ow1o = ow1;
+              oh1o = oh1;
             }
           }
           int cb = 0, r = 0, sft = 0;  // (tap, channel block) of chunk kc, tracked incrementally
@@ -608,8 +611,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   const int c2 = ck - g.k1_chunks + (a.k2_diag ? tn * (BN / BK) : 0);
                   if (FLAT)
                     tma_load_2d(dA, &tmap_a2, c2 * BK, tm * BM, &full[stage]);
-                  else if (IM2COL)
+                  else if (IM2COL) {
                     tma_load_im2col_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, 0, 0, &full[stage]);
+                    if (MT > 1 && nsub > 1)  // MODE 10: the second M sub-tile's downsample rows
+                      tma_load_im2col_4d(dA + A_STAGE_BYTES, &tmap_a2, c2 * BK, ow1o * a.stride2, oh1o * a.stride2, b1,
+                                         0, 0, &full[stage]);
+                  }
                   else
                     tma_load_4d(dA, &tmap_a2, c2 * BK, ow0 * a.stride2, oh0 * a.stride2, b0, &full[stage]);
                 } else if (FLAT) {
@@ -1396,6 +1403,22 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
 
 }  // namespace
 
+bool dual_m_ntiles_enabled() {  // HAPI_DUAL_M_NT=1: MODE 10 at BN = 256 also when Cout > 256 (experiment)
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M_NT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+bool dual_m_ds_enabled() {  // HAPI_DUAL_M_DS=1: ... also with the fused 1x1/s2 downsample source (experiment)
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M_DS");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool dual_m1x1_enabled() {  // HAPI_DUAL_M1X1=1: 1x1 convs with two M sub-tiles per weight chunk (MODE 11)
   static const bool on = [] {
     const char* e = std::getenv("HAPI_DUAL_M1X1");
@@ -1553,7 +1576,8 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   // ... and at BN = 256 (one accumulator buffer of 2 x 256 columns): the 3x3 convs of ResNet-50
   // stage 3 move 1.38 GB through L2 per launch at BN = 256 x 1 M tile (the weights re-read per
   // 128-pixel tile are two thirds of it); two M tiles per weight chunk cut that to ~0.9 GB
-  if (mode == 5 && bn == 256 && g.n_tiles == 1 && !a.res && a.k2_chunks == 0 && dual_m_enabled() && dual_m256_enabled())
+  if (mode == 5 && bn == 256 && !a.res && !a.k2_diag && dual_m_enabled() && dual_m256_enabled() &&
+      (g.n_tiles == 1 || dual_m_ntiles_enabled()) && (a.k2_chunks == 0 || dual_m_ds_enabled()))
     g.mt = 2;
   // 1x1 convs without a residual (every bottleneck's conv1) likewise: the K = 512..2048 weight
   // chunks are re-read per 128-row tile otherwise (ResNet-50 stage 3 conv1: 411 of 616 MB through

@@ -1916,17 +1916,19 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
 }
 
 static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
-                                        void* out);
+                                        void* out, bool ramp_fill);
 
 hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
-  hapi_status st = forward_host_enqueue(m, split_idx, images, batch, out);
+  hapi_status st = forward_host_enqueue(m, split_idx, images, batch, out, true);
   if (st != HAPI_OK) return st;
   return hapi_host_sync(m);
 }
 
 hapi_status hapi_prefix_forward_host_async(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
                                            void* out) {
-  return forward_host_enqueue(m, split_idx, images, batch, out);
+  // (no half-size first chunk: in a stream of calls the H2D of this call's first chunk overlaps
+  // the previous call's compute, so the fill the ramp shortens is not exposed)
+  return forward_host_enqueue(m, split_idx, images, batch, out, false);
 }
 
 hapi_status hapi_host_sync(hapi_model* m) {
@@ -1941,7 +1943,7 @@ hapi_status hapi_host_sync(hapi_model* m) {
 }
 
 static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
-                                        void* out) {
+                                        void* out, bool ramp_fill) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
@@ -1968,7 +1970,7 @@ static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const
       return !(e && e[0] == '0');
     }();
     uint64_t left = batch;
-    if (ramp && B >= 32 && batch >= 2 * B) {
+    if (ramp_fill && ramp && B >= 32 && batch >= 2 * B) {
       sizes.push_back(B / 2);
       left -= B / 2;
     }

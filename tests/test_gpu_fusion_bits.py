@@ -50,6 +50,8 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("resnet50", 21, 224, 3, "HAPI_DUAL_M256", None, "0"),  # ... im2col at BN = 256 (one TMEM buffer), stage 3/4
     ("resnet50", 21, 160, 3, "HAPI_DUAL_M256", None, "0"),  # ... odd M-tile count
     ("resnet50", 21, 224, 401, "HAPI_DUAL_M1X1", "1", None),  # opt-in 1x1 two-M-tile MODE 11 (needs >= 2 waves)
+    ("resnet50", 21, 224, 3, "HAPI_DUAL_M_NT", "1", None),    # MODE 10 at BN = 256 with several N tiles (stage 4)
+    ("resnet50", 21, 160, 3, "HAPI_DUAL_M_DS", "1", None),    # ... with the fused 1x1/s2 downsample source
     ("resnet50", 21, 96, 6, "HAPI_CLUSTER", "1", None),     # 2-CTA multicast weights (opt-in)
     ("resnet50", 21, 160, 3, "HAPI_CLUSTER", "1", None),    # ... odd M-tile count (OOB pair tile)
     ("resnet50", 21, 96, 6, "HAPI_SUB_STORE", None, "0"),   # pair output stored at stride 2 for the ds
