@@ -72,7 +72,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
   static constexpr int FIXED = 2 * SB_BYTES /*out staging*/ + BN * 4 /*bias*/ + 1024 /*align*/ + 1024 /*barriers*/;
-  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 2 * MAX_RES + 9) * 8 + 4 <= 1024, "barrier area");
+  static_assert((3 * MAX_B_STAGES + 2 * MAX_A_STAGES + 2 * MAX_RES + 17) * 8 + 4 <= 1024, "barrier area");
   static int stages(bool res) {
     int s = (SMEM_LIMIT - FIXED - (res ? 2 * SB_BYTES : 0)) / STAGE_BYTES;
     return s > MAX_STAGES ? MAX_STAGES : s;
@@ -196,8 +196,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // TMEM accumulator buffers: two (the epilogue of tile i overlaps the MMAs of tile i+1) unless
   // MT x BN x 2 exceeds the 512 columns -- MODE 10 at BN = 256 keeps one buffer of 2 x 256 columns
   // (the weight stream halves; the MMAs wait for each tile pair's drain)
-  constexpr int NACC = (MT * BN * 2 <= 512) ? 2 : 1;
-  constexpr int TMEM_ALLOC = NACC == 2 ? C::TMEM_COLS * MT : BN * MT;
+  // MODE 8 (the stem, N = 128): four buffers, so the MMAs run up to three pooled rows ahead of the
+  // epilogue / pooling chain (each pooled row costs that chain more than its 20 MMAs)
+  constexpr int NACC = MODE == 8 ? 4 : (MT * BN * 2 <= 512) ? 2 : 1;
+  constexpr int TMEM_ALLOC = MODE == 8 ? 512 : NACC == 2 ? C::TMEM_COLS * MT : BN * MT;
   constexpr bool TMA_A = (FLAT || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   // 1x1 TMA tiles (mode 3): the epilogue stores per-warp [32 x 32] boxes through the 7th map
@@ -224,14 +226,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* afull = empty + MAX_B_STAGES;    // mode 6 halo ring
   uint64_t* aempty = afull + MAX_A_STAGES;
   uint64_t* tfull = aempty + MAX_A_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* rfull = tempty + 2;
+  uint64_t* tempty = tfull + 4;
+  uint64_t* rfull = tempty + 4;
   uint64_t* rempty = rfull + MAX_RES;
   uint64_t* bres = rempty + MAX_RES;         // resident weights landed
   uint64_t* lfull = bres + 1;                // mode 7: raw A tile landed (before the transform)
   uint64_t* pready = lfull + MAX_B_STAGES;   // mode 8: stem rows of a tile in the ring
-  uint64_t* pfree = pready + 2;              // mode 8: pooling of a tile done (its ring rows free)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfree + 2);
+  uint64_t* pfree = pready + 4;              // mode 8: pooling of a tile done (its ring rows free)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pfree + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&afull[i], 1);
       mbar_init(&aempty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], (MODE == 4 && g.pool2) ? NUM_EPI_THREADS / 2 : NUM_EPI_THREADS);
     }
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&rempty[i], NUM_EPI_THREADS);
     }
     mbar_init(bres, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&pready[i], NUM_EPI_THREADS);
       mbar_init(&pfree[i], M8_POOL_THREADS);
     }
@@ -381,9 +383,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int pt = task / g.nseg, seg = task - pt * g.nseg;
       const int img = pt / g.strips, pair = pt - img * g.strips;
       const int po = seg * g.seg_rows - 1 + t;
-      mbar_wait(&pready[it & 1], (it >> 1) & 1);
+      mbar_wait(&pready[it & 3], (it >> 2) & 1);
       if (t > 0 && po < g.ph) {  // the warm-up tile only seeds the vertical pool; rows past ph are dead
-        const uint32_t vbuf = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2));
+        const uint32_t vbuf = smem_u32(sY) + (uint32_t)((it & 3) * (g.ring_bytes / 4));
         __nv_bfloat16* yrow = yb + (((long long)img * g.ph + po) * g.pw + 2 * pair * g.pq) * a.y_ld;
         const int qlim = g.pw - 2 * pair * g.pq;
 #pragma unroll
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           *reinterpret_cast<uint4*>(yrow + (long long)qcol[i] * a.y_ld + cgo[i]) = make_uint4(mx[0], mx[1], mx[2], mx[3]);
         }
       }
-      mbar_arrive(&pfree[it & 1]);
+      mbar_arrive(&pfree[it & 3]);
       if (++t == g.tlen) {
         t = 0;
         task += gridDim.x;
@@ -432,7 +434,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // whose only use is to leave relu(stem row 2 h0 - 1) in prev for the segment's first row
     int t = 0, task = blockIdx.x;
     for (int it = 0; task < g.n_tasks; ++it) {
-      const int acc = it & 1;
+      const int acc = it & 3;
       const int pt = task / g.nseg;
       const int pair = pt % g.strips;
       const int po = (task - pt * g.nseg) * g.seg_rows - 1 + t;
@@ -440,7 +442,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const bool valid = live && stem_col >= 0 && stem_col < a.OW;
       const bool valid0 = valid && 2 * po >= 0 && 2 * po < a.OH;  // padding positions are -inf
       const bool valid1 = valid && 2 * po + 1 >= 0 && 2 * po + 1 < a.OH;
-      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      mbar_wait(&tfull[acc], (it >> 2) & 1);
       tc_fence_after();
       uint32_t v0[32], v1[32];
       const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + gsel * 32;
@@ -449,9 +451,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      mbar_wait(&pfree[it & 1], ((it >> 1) & 1) ^ 1);
+      mbar_wait(&pfree[it & 3], ((it >> 2) & 1) ^ 1);
       if (live) {
-        const uint32_t dst = smem_u32(sY) + (uint32_t)((it & 1) * (g.ring_bytes / 2) + row * 128);
+        const uint32_t dst = smem_u32(sY) + (uint32_t)((it & 3) * (g.ring_bytes / 4) + row * 128);
 #pragma unroll
         for (int c4 = 0; c4 < 4; ++c4) {
           uint32_t o[4];
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(&pready[it & 1]);
+      mbar_arrive(&pready[it & 3]);
       if (++t == g.tlen) {
         t = 0;
         task += gridDim.x;
@@ -769,8 +771,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (TMA_A && g.b_res) mbar_wait(bres, 0);
       int iter = 0;
       for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
-        const int acc = NACC == 2 ? (iter & 1) : 0;
-        const uint32_t acc_phase = NACC == 2 ? ((iter >> 1) & 1) : (iter & 1);
+        const int acc = iter % NACC;
+        const uint32_t acc_phase = (iter / NACC) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * MT * BN;
@@ -1518,7 +1520,7 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
       g.a_stage_bytes = 2 * pstride;
     }
     g.a_stages = 4;
-    g.ring_bytes = 2 * 2 * g.we * 128;         // two buffers of vertically pooled rows
+    g.ring_bytes = 4 * 2 * g.we * 128;         // four buffers of vertically pooled rows
     g.tma_out = 0;
   } else if (mode == 6) {
     // halo tile: full output rows (wb = OW), hb rows, one image; extended width we = OW + KW - 1
