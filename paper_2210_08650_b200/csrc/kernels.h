@@ -142,6 +142,25 @@ struct PairMaps {
 };
 cudaError_t conv_pair_launch(const PairArgs& a, const PairMaps& mp, int n2, int num_sms, cudaStream_t st);
 
+// A whole identity bottleneck (1x1 C->64, 3x3 64->64, 1x1 64->C + x, each + folded BN + ReLU) on
+// a CTA pair (conv_block.cu): x is read once, t1/t2 stay on chip.  C <= 256, W <= 62.
+struct BlockArgs {
+  int N, H, W, C;        // x / y: NHWC [N][H][W][C] bf16
+  const void* x; int x_ld;
+  void* y; int y_ld;     // must not alias x
+  const float* b1;       // [64]
+  const float* b2;       // [64]
+  const float* b3;       // [C]
+};
+struct BlockMaps {
+  const CUtensorMap* x;   // 4D {C, W, H, N} over x, box {64, 64, 2, 1}, SW128
+  const CUtensorMap* w1;  // 2D over W1 [64][C], box {64, 32}, SW128
+  const CUtensorMap* w2;  // 2D over W2 [64][576] (taps (r, s) x 64 channels), box {64, 32}, SW128
+  const CUtensorMap* w3;  // 2D over W3 [C][64], box {64, C/2}, SW128
+};
+cudaError_t conv_block_launch(const BlockArgs& a, const BlockMaps& mp, int num_sms, cudaStream_t st);
+int conv_block_smem_bytes(int C);
+
 int conv_tc_pick_bn(int cout);
 int conv_tc_store_cols(int bn);  // columns per epilogue TMA box (64, or bn if smaller)
 void conv_tc_spatial_tile(int OH, int OW, int N, int* wb, int* hb, int* nb);

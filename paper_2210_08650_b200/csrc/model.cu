@@ -103,6 +103,14 @@ bool stem_pool_enabled() {
   return on;
 }
 
+bool block_enabled() {  // HAPI_BLOCK=1: whole identity bottlenecks on a CTA pair (conv_block.cu)
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_BLOCK");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 bool pair_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_PAIR");
@@ -186,7 +194,7 @@ struct ConvW {
   bool res_identity = false;         // K2 columns are an identity block: + residual inside the GEMM
 };
 
-enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT, OP_PAIR, OP_UNPACK };
+enum OpType { OP_PACK_IN, OP_CONV, OP_POOL, OP_ADAPTIVE, OP_BNACT, OP_PACK_OUT, OP_PAIR, OP_UNPACK, OP_BLOCK };
 
 struct View {
   int buf = -1;       // -1: external (caller out, or caller images for PACK_IN input)
@@ -231,6 +239,10 @@ struct Op {
   bool sub_out = false;
   int full_h = 0, full_w = 0;
   bool pool2 = false;            // mode-4 conv with the following 2x2/s2 maxpool in its epilogue (out = pooled)
+  // OP_BLOCK (conv_block.cu): conv = conv1, conv2 = conv2, conv3 = conv3 of an identity
+  // bottleneck; in = x, out = block output; maps over x and the three weight tensors
+  int conv3 = -1;
+  CUtensorMap bmap_x, bmap_w1, bmap_w2, bmap_w3;
   int in2_stride = 0;            // 0: the conv's own stride2
 };
 
@@ -1014,6 +1026,38 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         const std::string& p = md.name;
         const int OH = out_dim(cur.H, 3, md.stride, 1), OW = out_dim(cur.W, 3, md.stride, 1);
         View x = cur;
+        if (md.kind == MK_BOTTLENECK && m->bf16 && !md.ds && md.stride == 1 && md.planes == 64 && md.cout == cur.C &&
+            cur.C % 64 == 0 && cur.C <= 256 && cur.W <= 62 && cur.ld == cur.C && cur.coff == 0 && block_enabled()) {
+          // the whole block on a CTA pair: x read once (the residual from L2), t1/t2 on chip
+          ConvSpec c1, c2, c3;
+          c1.wname = p + ".conv1.weight"; c1.fold_bn = p + ".bn1";
+          c1.cin = md.cin; c1.cout = 64; c1.k = 1; c1.cs = x.C;
+          c2.wname = p + ".conv2.weight"; c2.fold_bn = p + ".bn2";
+          c2.cin = 64; c2.cout = 64; c2.k = 3; c2.pad = 1; c2.cs = 64;
+          c3.wname = p + ".conv3.weight"; c3.fold_bn = p + ".bn3";
+          c3.cin = 64; c3.cout = md.cout; c3.k = 1; c3.cs = 64;
+          int i1, i2, i3;
+          if ((st = make_conv(m, c1, &i1)) != HAPI_OK || (st = make_conv(m, c2, &i2)) != HAPI_OK ||
+              (st = make_conv(m, c3, &i3)) != HAPI_OK)
+            return st;
+          Op o;
+          o.t = OP_BLOCK;
+          o.in = x;
+          o.out = b.compact(md.cout, cur.H, cur.W);
+          o.conv = i1; o.conv2 = i2; o.conv3 = i3;
+          o.kind = 0;
+          const double px = (double)cur.H * cur.W;
+          o.flops = (m->convs[i1].real_flops_per_px + m->convs[i2].real_flops_per_px + m->convs[i3].real_flops_per_px) * px;
+          o.bytes = 2.0 * px * md.cout * m->es;
+          char d[160];
+          std::snprintf(d, sizeof(d), "block[%s 1x1 C%d->64, 3x3 64->64, 1x1 64->%d +res] %dx%d (CTA pair)", p.c_str(),
+                        x.C, md.cout, cur.H, cur.W);
+          o.desc = d;
+          b.emit(o);
+          cur = o.out;
+          i += 1;
+          break;
+        }
         View t;
         if (md.kind == MK_BOTTLENECK) {
           View t1 = b.compact(md.planes, cur.H, cur.W);
@@ -1422,6 +1466,19 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
     case OP_PACK_OUT:
       e = pack_output_launch(vptr(m, p, o.in, out), nb, o.in.H * o.in.W, o.in.C, o.in.ld, out, isb, st);
       break;
+    case OP_BLOCK: {
+      BlockArgs a;
+      a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = o.in.C;
+      a.x = vptr(m, p, o.in, out); a.x_ld = o.in.ld;
+      a.y = vptr(m, p, o.out, out); a.y_ld = o.out.ld;
+      a.b1 = m->convs[o.conv].bias;
+      a.b2 = m->convs[o.conv2].bias;
+      a.b3 = m->convs[o.conv3].bias;
+      BlockMaps mp;
+      mp.x = &o.bmap_x; mp.w1 = &o.bmap_w1; mp.w2 = &o.bmap_w2; mp.w3 = &o.bmap_w3;
+      e = conv_block_launch(a, mp, m->num_sms, st);
+      break;
+    }
   }
   if (e != cudaSuccess)
     return set_error(HAPI_ERR_CUDA, "launch of %s failed: %s", o.desc.empty() ? "op" : o.desc.c_str(), cudaGetErrorString(e));
@@ -1504,6 +1561,27 @@ hapi_status finalize_tmaps(hapi_model* m) {
   if (!m->bf16) return HAPI_OK;
   for (Plan& p : m->plans) {
     for (Op& o : p.ops) {
+      if (o.t == OP_BLOCK) {
+        const ConvW &w1 = m->convs[o.conv], &w2 = m->convs[o.conv2], &w3 = m->convs[o.conv3];
+        const cuuint64_t ld = (cuuint64_t)o.in.ld * 2;
+        cuuint64_t xd[4] = {(cuuint64_t)o.in.C, (cuuint64_t)o.in.W, (cuuint64_t)o.in.H, (cuuint64_t)m->d.max_batch};
+        cuuint64_t xs[3] = {ld, ld * o.in.W, ld * o.in.W * o.in.H};
+        cuuint32_t xb[4] = {64, 64, 2, 1};
+        cuuint32_t e4[4] = {1, 1, 1, 1};
+        hapi_status st = encode_bf16(&o.bmap_x, 4, vptr(m, p, o.in, nullptr), xd, xs, xb, e4, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     o.desc + " x");
+        auto wmap = [&](CUtensorMap* mp, const ConvW& w, int rows) {
+          cuuint64_t dd[2] = {(cuuint64_t)w.Kp, (cuuint64_t)w.cout};
+          cuuint64_t ss[1] = {(cuuint64_t)w.Kp * 2};
+          cuuint32_t bb[2] = {64, (cuuint32_t)rows};
+          return encode_bf16(mp, 2, w.w, dd, ss, bb, e4, CU_TENSOR_MAP_SWIZZLE_128B, o.desc + " w");
+        };
+        if (st == HAPI_OK) st = wmap(&o.bmap_w1, w1, 32);
+        if (st == HAPI_OK) st = wmap(&o.bmap_w2, w2, 32);
+        if (st == HAPI_OK) st = wmap(&o.bmap_w3, w3, w3.cout / 2);
+        if (st != HAPI_OK) return st;
+        continue;
+      }
       if (o.t != OP_CONV && o.t != OP_PAIR) continue;
       const ConvW& w = m->convs[o.conv];
       hapi_status st = HAPI_OK;
@@ -2019,7 +2097,7 @@ hapi_status hapi_plan_describe(const hapi_model* m, uint32_t split_idx, uint32_t
   if (split_idx < m->d.min_split || split_idx > m->d.max_split) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx");
   const Plan& p = m->plans[split_idx - m->d.min_split];
   if (op >= p.ops.size()) return set_error(HAPI_ERR_INVALID_ARGUMENT, "op index");
-  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out", "pair", "unpack"};
+  static const char* names[] = {"pack_in", "conv", "pool", "adaptive_avgpool", "bn_act", "pack_out", "pair", "unpack", "block"};
   const Op& o = p.ops[op];
   std::snprintf(buf, cap, "%s%s%s", o.desc.empty() ? names[o.t] : o.desc.c_str(), o.out.buf < 0 ? " ->out" : "",
                 o.nchw_out ? "(nchw)" : "");

@@ -1,0 +1,56 @@
+"""The fused identity-bottleneck kernel (conv_block.cu: a whole ResNet-50 stage-1 block on a CTA
+pair, t1/t2 on chip, the residual re-read from L2) against the oracle at every split that ends
+inside or after the fused blocks, at 96 px (24x24 stage-1 maps, odd image count: the CTA pair's
+second image is a phantom) and at 224 px (56x56), and against the unfused launches."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+_SNIPPET = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import hapi_inputs
+from tests.gpu_helpers import gpu_forward, oracle_all
+from tests.parity_check import check_close
+arch, size, n = "resnet50", {size}, {n}
+P = hapi_inputs.params(arch, 51)
+x = hapi_inputs.images(n, 52, size, size)
+import paper_2210_08650_b200 as H
+m = H.Model(arch, "bf16", list(P.values()), n, 5, 22, in_h=size, in_w=size)
+info = m.plan_info(21)
+assert any(d.startswith("block[") for d in info["desc"]) == {expect_block}, info["desc"]
+outs = {{}}
+for s in {splits}:
+    y, _ = gpu_forward(arch, "bf16", s, x, P, model=m)
+    check_close(y, oracle_all(arch, 51, 52, n, size, size, upto=s)[s - 1], "bf16", "block s=%d %dpx" % (s, size))
+    outs[s] = y
+np.savez({out!r}, **{{str(k): v for k, v in outs.items()}})
+print("ok")
+"""
+
+
+def _run(tmp_path, flag, size, n, splits):
+    out = str(tmp_path / f"b{flag}_{size}.npz")
+    env = dict(os.environ)
+    env["HAPI_BLOCK"] = flag
+    code = _SNIPPET.format(root=ROOT, size=size, n=n, splits=splits, out=out, expect_block=(flag == "1"))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+    return np.load(out)
+
+
+@pytest.mark.parametrize("size,n", [(96, 3), (224, 4)])
+def test_block_kernel_matches_oracle_and_unfused(tmp_path, size, n):
+    splits = [5, 6, 7, 8, 21]
+    fused = _run(tmp_path, "1", size, n, splits)
+    plain = _run(tmp_path, "0", size, n, splits)
+    for s in splits:
+        a, b = fused[str(s)], plain[str(s)]
+        # same arithmetic up to the fp32 summation order of the residual (epilogue vs in-GEMM)
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-2, s
