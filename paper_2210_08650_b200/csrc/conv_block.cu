@@ -23,8 +23,10 @@
 // Every TMEM lane is one tile position in all three GEMMs, so an epilogue thread handles the
 // same position through E1 (t1 row slot), E2 (t2) and E3 (+ residual, global store).
 //
-// Warps (320 threads per CTA): 0-7 epilogue (lane quarter w & 3, column half w >> 2), 8 TMA
-// producer (weights once, then the x chunks), 9 TMEM allocator + (leader) MMA issuer.
+// Warps (448 threads per CTA): 0-7 E3 (lane quarter w & 3, column half w >> 2 of the C output
+// columns), 8-11 E1 and E2 (lane quarter w & 3, all 64 columns) -- separate warps so the
+// residual-and-store epilogue of tile p overlaps the t1/t2 epilogues of tiles p+1, p+2 --,
+// 12 TMA producer (weights once, then the x chunks), 13 TMEM allocator + (leader) MMA issuer.
 #include <cuda_bf16.h>
 
 #include "kernels.h"
@@ -34,9 +36,10 @@ namespace hapi {
 namespace {
 using namespace tcx;
 
-constexpr int B_THREADS = 320;
-constexpr int B_PROD_WARP = 8;
-constexpr int B_MMA_WARP = 9;
+constexpr int B_THREADS = 448;
+constexpr int B_E12_WARP0 = 8;          // warps 8-11: E1 and E2 (one per TMEM lane quarter)
+constexpr int B_PROD_WARP = 12;
+constexpr int B_MMA_WARP = 13;
 constexpr int B_XS = 4;                 // x ring stages (one 64-channel chunk of a tile each)
 constexpr int B_SLOTS = 6;              // t1 row slots (+2 shadows)
 constexpr int B_ROW = 64 * 128;         // one t1 row slot: 64 positions x 64 ch bf16
@@ -56,7 +59,7 @@ struct BlkLayout {
     o += 1024;                                     // guard before the t1 ring (position -1)
     L.t1 = o; o += (B_SLOTS + 2) * B_ROW + 1024;   // ring + 2 shadows + guard after
     L.t2 = o; o += B_CHUNK;
-    L.bias3 = o; o += C * 4;
+    L.bias3 = o; o += C * 4 + 128 * 4;              // b3, then b1 | b2
     L.bars = o; o += 512;
     L.total = o + 1024;                            // + alignment slack
     return L;
@@ -184,15 +187,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     mbar_init(&bars[WFULL], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars[D1FULL + i], 1);
-      mbar_init(&bars[D1EMPTY + i], 16);
+      mbar_init(&bars[D1EMPTY + i], 8);
       mbar_init(&bars[D2FULL + i], 1);
-      mbar_init(&bars[D2EMPTY + i], 16);
+      mbar_init(&bars[D2EMPTY + i], 8);
       mbar_init(&bars[C2DONE + i], 1);
     }
     mbar_init(&bars[D3FULL], 1);
     mbar_init(&bars[D3EMPTY], 16);
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[T1READY + i], 16);
-    mbar_init(&bars[T2READY], 16);
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[T1READY + i], 8);
+    mbar_init(&bars[T2READY], 8);
     mbar_init(&bars[C3DONE], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -202,6 +205,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     *reinterpret_cast<uint4*>(base + L.t1 + (B_SLOTS + 2) * B_ROW + i * 16) = make_uint4(0, 0, 0, 0);
   }
   for (int i = threadIdx.x; i < a.C; i += B_THREADS) sB3[i] = a.b3 ? __ldg(a.b3 + i) : 0.f;
+  for (int i = threadIdx.x; i < 128; i += B_THREADS)
+    sB3[a.C + i] = i < 64 ? (a.b1 ? __ldg(a.b1 + i) : 0.f) : (a.b2 ? __ldg(a.b2 + i - 64) : 0.f);
   if (warp == B_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
@@ -333,39 +338,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
         }
       }
     }
-  } else if (warp < 8) {
-    // ================================================================ epilogues
-    const int quarter = warp & 3, gsel = warp >> 2;
+  } else if (warp >= B_E12_WARP0 && warp < B_E12_WARP0 + 4) {
+    // ================================================================ E1 / E2 warps
+    const int quarter = warp & 3;
     const int row = quarter * 32 + lane;        // TMEM lane = tile position
     const int ri = row >> 6, pos = row & 63;    // row in tile, padded position
     const int col = pos - 1;
     const bool col_ok = col >= 0 && col < a.W;
     const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
-    float b1[32], b2[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      b1[j] = a.b1 ? __ldg(a.b1 + gsel * 32 + j) : 0.f;
-      b2[j] = a.b2 ? __ldg(a.b2 + gsel * 32 + j) : 0.f;
-    }
+    const uint32_t sb1 = smem_u32(sB3 + a.C), sb2 = sb1 + 64 * 4;
     const uint32_t t1ready_l = mapa_leader(lbar(T1READY));
     const uint32_t t2ready_l = mapa_leader(lbar(T2READY));
     const uint32_t d1empty_l = mapa_leader(lbar(D1EMPTY));
     const uint32_t d2empty_l = mapa_leader(lbar(D2EMPTY));
-    const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
     auto warp_arrive = [&](uint32_t cluster_bar) {
       __syncwarp();
       if (lane == 0) arrive_remote(cluster_bar);
     };
-    const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
-    __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
-    int n1 = 0, n2 = 0, n3 = 0;
+    // relu(v + bias) of 32 accumulator columns (bias from smem) -> 16 bf16x2
+    auto act32 = [&](const uint32_t (&v)[32], uint32_t bias_addr, bool ok, uint32_t (&o)[16]) {
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const float4 q0 = lds_f4(bias_addr + c4 * 32), q1 = lds_f4(bias_addr + c4 * 32 + 16);
+        const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          o[c4 * 4 + j] = ok ? cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * j]) + bb[2 * j],
+                                               __uint_as_float(v[c4 * 8 + 2 * j + 1]) + bb[2 * j + 1])
+                             : 0u;
+      }
+    };
+    int n1 = 0, n2 = 0;
     Seg s;
     for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
       const int n = s.pb - s.pa + 1;
       const int c2b = n2;  // C2s issued before this segment
-      const int img = 2 * s.ip + (int)rank;
-      const bool img_ok = img < a.N;
-      for (int k = 0; k <= n + 3; ++k) {
+      for (int k = 0; k <= n + 2; ++k) {
         if (k <= n + 1) {
           // ---- E1(q): relu(D1 + b1) -> t1 row slot of row 2q + ri (zero outside the image)
           const int q = s.pa - 1 + k;
@@ -374,8 +382,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           const int b = n1 & 1;
           mbar_wait(&bars[D1FULL + b], (n1 >> 1) & 1);
           tc_fence_after();
-          uint32_t v[32];
-          tmem_ld32(lanebase + b * 64 + gsel * 32, v);
+          uint32_t v0[32], v1[32];
+          tmem_ld32(lanebase + b * 64, v0);
+          tmem_ld32(lanebase + b * 64 + 32, v1);
           tmem_wait_ld();
           tc_fence_before();
           warp_arrive(d1empty_l + 8u * b);
@@ -387,22 +396,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
             if (issued > 0) mbar_wait(&bars[C2DONE + ((issued - 1) & 1)], ((issued - 1) >> 1) & 1);
           }
           const int slot = ((r + 1) % B_SLOTS + B_SLOTS) % B_SLOTS;
-          uint32_t o[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            o[j] = ok ? cvt_relu_bf16x2(__uint_as_float(v[2 * j]) + b1[2 * j], __uint_as_float(v[2 * j + 1]) + b1[2 * j + 1])
-                      : 0u;
           const uint32_t rowaddr = sbase + L.t1 + slot * B_ROW + pos * 128;
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            const uint32_t off = (((gsel * 4 + c4) ^ (pos & 7)) << 4);
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + off), "r"(o[4 * c4]),
-                         "r"(o[4 * c4 + 1]), "r"(o[4 * c4 + 2]), "r"(o[4 * c4 + 3])
-                         : "memory");
-            if (slot < 2)  // shadow copy after the ring (keeps every 4-row window contiguous)
-              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + B_SLOTS * B_ROW + off),
-                           "r"(o[4 * c4]), "r"(o[4 * c4 + 1]), "r"(o[4 * c4 + 2]), "r"(o[4 * c4 + 3])
+          for (int h = 0; h < 2; ++h) {
+            uint32_t o[16];
+            act32(h ? v1 : v0, sb1 + h * 128, ok, o);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const uint32_t off = (((h * 4 + c4) ^ (pos & 7)) << 4);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + off), "r"(o[4 * c4]),
+                           "r"(o[4 * c4 + 1]), "r"(o[4 * c4 + 2]), "r"(o[4 * c4 + 3])
                            : "memory");
+              if (slot < 2)  // shadow copy after the ring (keeps every 4-row window contiguous)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + B_SLOTS * B_ROW + off),
+                             "r"(o[4 * c4]), "r"(o[4 * c4 + 1]), "r"(o[4 * c4 + 2]), "r"(o[4 * c4 + 3])
+                             : "memory");
+            }
           }
           fence_proxy_async_smem();
           warp_arrive(t1ready_l + 8u * (n1 & 3));
@@ -413,68 +422,100 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           const int b = n2 & 1;
           mbar_wait(&bars[D2FULL + b], (n2 >> 1) & 1);
           tc_fence_after();
-          uint32_t v[32];
-          tmem_ld32(lanebase + 128 + b * 64 + gsel * 32, v);
+          uint32_t v0[32], v1[32];
+          tmem_ld32(lanebase + 128 + b * 64, v0);
+          tmem_ld32(lanebase + 128 + b * 64 + 32, v1);
           tmem_wait_ld();
           tc_fence_before();
           warp_arrive(d2empty_l + 8u * b);
           if (n2 >= 1) mbar_wait(&bars[C3DONE], (n2 - 1) & 1);  // C3 of the previous tile read t2
           const uint32_t rowaddr = sbase + L.t2 + row * 128;
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {
-            uint32_t o[4];
+          for (int h = 0; h < 2; ++h) {
+            uint32_t o[16];
+            act32(h ? v1 : v0, sb2 + h * 128, true, o);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const int c = c4 * 8 + 2 * j;
-              o[j] = cvt_relu_bf16x2(__uint_as_float(v[c]) + b2[c], __uint_as_float(v[c + 1]) + b2[c + 1]);
-            }
-            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + (((gsel * 4 + c4) ^ (row & 7)) << 4)),
-                         "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
-                         : "memory");
+            for (int c4 = 0; c4 < 4; ++c4)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + (((h * 4 + c4) ^ (row & 7)) << 4)),
+                           "r"(o[4 * c4]), "r"(o[4 * c4 + 1]), "r"(o[4 * c4 + 2]), "r"(o[4 * c4 + 3])
+                           : "memory");
           }
           fence_proxy_async_smem();
           warp_arrive(t2ready_l);
           ++n2;
         }
-        if (k >= 4) {
-          // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
-          const int p = s.pa + k - 4;
-          const int r = 2 * p + ri;
-          const bool ok = img_ok && col_ok && r < a.H;
-          mbar_wait(&bars[D3FULL], n3 & 1);
-          tc_fence_after();
-          const long long pix = ((long long)img * a.H + r) * a.W + col;
-          const __nv_bfloat16* xr = xg + pix * a.x_ld;
-          __nv_bfloat16* yr = yg + pix * a.y_ld;
+      }
+    }
+  } else if (warp < 8) {
+    // ================================================================ E3 warps
+    const int quarter = warp & 3, gsel = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int ri = row >> 6, pos = row & 63;
+    const int col = pos - 1;
+    const bool col_ok = col >= 0 && col < a.W;
+    const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
+    const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
+    __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
+    const int nsub = a.C / 64;                  // 32-column blocks of this thread's half
+    int n3 = 0;
+    Seg s;
+    for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
+      const int img = 2 * s.ip + (int)rank;
+      const bool img_ok = img < a.N;
+      for (int p = s.pa; p <= s.pb; ++p) {
+        // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
+        const int r = 2 * p + ri;
+        const bool ok = img_ok && col_ok && r < a.H;
+        const long long pix = ((long long)img * a.H + (ok ? r : 0)) * a.W + (ok ? col : 0);
+        const uint4* xr = reinterpret_cast<const uint4*>(xg + pix * a.x_ld + gsel * (a.C / 2));
+        __nv_bfloat16* yr = yg + pix * a.y_ld + gsel * (a.C / 2);
+        // the residual of the first 32-column block is in flight while the MMA finishes
+        uint4 res[4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) res[q4] = ok ? __ldg(xr + q4) : make_uint4(0, 0, 0, 0);
+        mbar_wait(&bars[D3FULL], n3 & 1);
+        tc_fence_after();
 #pragma unroll 1
-          for (int sub = 0; sub < a.C / 64; ++sub) {
-            const int c0 = gsel * (a.C / 2) + sub * 32;
-            uint32_t v[32];
-            tmem_ld32(lanebase + 256 + c0, v);
-            tmem_wait_ld();
-            if (ok) {
-              uint32_t o[16];
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                const uint4 u = __ldg(reinterpret_cast<const uint4*>(xr + c0) + q4);
-                const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                  const float2 f = unpack_bf16x2(uu[h]);
-                  const int c = q4 * 8 + 2 * h;
-                  o[q4 * 4 + h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + sB3[c0 + c] + f.x,
-                                                  __uint_as_float(v[c + 1]) + sB3[c0 + c + 1] + f.y);
-                }
-              }
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4)
-                *reinterpret_cast<uint4*>(yr + c0 + q4 * 8) = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
-            }
+        for (int sub = 0; sub < nsub; ++sub) {
+          const int c0 = sub * 32;
+          uint32_t v[32];
+          tmem_ld32(lanebase + 256 + gsel * (a.C / 2) + c0, v);
+          tmem_wait_ld();
+          if (sub == nsub - 1) {  // D3 drained: the next C3 may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_remote(d3empty_l);
           }
-          tc_fence_before();
-          warp_arrive(d3empty_l);
-          ++n3;
+          uint4 cur[4];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) cur[q4] = res[q4];
+          if (sub + 1 < nsub) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) res[q4] = ok ? __ldg(xr + (sub + 1) * 4 + q4) : make_uint4(0, 0, 0, 0);
+          }
+          if (ok) {
+            uint32_t o[16];
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              const uint32_t uu[4] = {cur[q4].x, cur[q4].y, cur[q4].z, cur[q4].w};
+              const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + c0 + q4 * 8);
+              const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
+              const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const float2 f = unpack_bf16x2(uu[h]);
+                const int c = q4 * 8 + 2 * h;
+                o[q4 * 4 + h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + bb[2 * h] + f.x,
+                                                __uint_as_float(v[c + 1]) + bb[2 * h + 1] + f.y);
+              }
+            }
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4)
+              *reinterpret_cast<uint4*>(yr + c0 + q4 * 8) = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
+          }
         }
+        ++n3;
       }
     }
   }
