@@ -15,7 +15,7 @@
 //
 // Tiles: one tile = two image rows x 64 positions (position p = column p - 1; 0 and >= W+1
 // are zero padding), M = 128 per CTA.  Rolling rows: a segment of row pairs [pa, pb] of one
-// image pair is computed as   step k:  C1(pa - 1 + k)   C2(pa + k - 3)   C3(pa + k - 4)
+// image pair is computed as   step k:  C2(pa + k - 3)   C1(pa - 1 + k)   C3(pa + k - 4)
 // (the C1 tiles -1 and PR produce the zero rows above and below the image).  t1 lives in a
 // ring of six 8 KB row slots (row r -> slot (r + 1) mod 6) plus shadow copies of slots 0, 1,
 // so the four rows 2p-1 .. 2p+2 conv2 reads are always one contiguous window; each 3x3 tap is
@@ -262,32 +262,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
         const int n = s.pb - s.pa + 1;
         const int c1b = n1;  // C1 sequence number of this segment's first tile (row pair pa - 1)
         for (int k = 0; k <= n + 3; ++k) {
-          if (k <= n + 1) {
-            // C1(q = pa - 1 + k): x chunks x W1 half -> D1[n1 & 1]
-            const int b = n1 & 1;
-            mbar_wait_cl(&bars[D1EMPTY + b], ((n1 >> 1) & 1) ^ 1);
-            tc_fence_after();
-            for (int c = 0; c < kc1; ++c) {
-              mbar_wait_cl(&bars[XFULL + st], ph);
-              tc_fence_after();
-              if (elect_one()) {
-                const uint64_t ad = make_sdesc(sbase + L.x + st * B_CHUNK);
-                const uint64_t bd = make_sdesc(sbase + L.w1 + c * 4096);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma2(tmem + b * 64, ad + 2 * kk, bd + 2 * kk, id64, (c | kk) != 0);
-                commit2(&bars[XEMPTY + st]);
-                if (c == kc1 - 1) commit2(&bars[D1FULL + b]);
-              }
-              __syncwarp();
-              if (++st == B_XS) { st = 0; ph ^= 1; }
-            }
-            ++n1;
-          }
           if (k >= 3 && k <= n + 2) {
             // C2(p = pa + k - 3): t1 window rows 2p-1 .. 2p+2, written by the E1s of C1 tiles
             // p - 1 .. p + 1 (in order, so waiting for the last suffices)
             const int p = s.pa + k - 3;
-            const int need = c1b + (p + 1) - (s.pa - 1);  // sequence number of C1(p + 1)
+            const int need = c1b + (p + 1) - (s.pa - 1);  // sequence number of C1(p + 1), issued last step
             mbar_wait_cl(&bars[T1READY + (need & 3)], (need >> 2) & 1);
             const int b = n2 & 1;
             mbar_wait_cl(&bars[D2EMPTY + b], ((n2 >> 1) & 1) ^ 1);
@@ -318,6 +297,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
             }
             __syncwarp();
             ++n2;
+          }
+          if (k <= n + 1) {
+            // C1(q = pa - 1 + k): x chunks x W1 half -> D1[n1 & 1]
+            const int b = n1 & 1;
+            mbar_wait_cl(&bars[D1EMPTY + b], ((n1 >> 1) & 1) ^ 1);
+            tc_fence_after();
+            for (int c = 0; c < kc1; ++c) {
+              mbar_wait_cl(&bars[XFULL + st], ph);
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t ad = make_sdesc(sbase + L.x + st * B_CHUNK);
+                const uint64_t bd = make_sdesc(sbase + L.w1 + c * 4096);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) mma2(tmem + b * 64, ad + 2 * kk, bd + 2 * kk, id64, (c | kk) != 0);
+                commit2(&bars[XEMPTY + st]);
+                if (c == kc1 - 1) commit2(&bars[D1FULL + b]);
+              }
+              __syncwarp();
+              if (++st == B_XS) { st = 0; ph ^= 1; }
+            }
+            ++n1;
           }
           if (k >= 4) {
             // C3(p = pa + k - 4): t2 x W3 half -> D3
