@@ -457,66 +457,73 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
     const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
     __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
-    const int nsub = a.C / 64;                  // 32-column blocks of this thread's half
+    const int nsub = a.C / 64;                  // 32-column blocks of this thread's half (<= 4)
+    // the residual of a tile (this thread's C/2 channels, <= 16 x 16 B) is loaded one tile
+    // ahead: its L2 round trip overlaps the wait for the next accumulator
+    uint4 res[16];
+    auto load_res = [&](int img, int p, bool& ok, const uint4*& xr, __nv_bfloat16*& yr) {
+      const int r = 2 * p + ri;
+      ok = img < a.N && col_ok && r < a.H;
+      const long long pix = ((long long)img * a.H + (ok ? r : 0)) * a.W + (ok ? col : 0);
+      xr = reinterpret_cast<const uint4*>(xg + pix * a.x_ld + gsel * (a.C / 2));
+      yr = yg + pix * a.y_ld + gsel * (a.C / 2);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) res[j] = (ok && j < nsub * 4) ? __ldg(xr + j) : make_uint4(0, 0, 0, 0);
+    };
     int n3 = 0;
     Seg s;
-    for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
-      const int img = 2 * s.ip + (int)rank;
-      const bool img_ok = img < a.N;
-      for (int p = s.pa; p <= s.pb; ++p) {
-        // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
-        const int r = 2 * p + ri;
-        const bool ok = img_ok && col_ok && r < a.H;
-        const long long pix = ((long long)img * a.H + (ok ? r : 0)) * a.W + (ok ? col : 0);
-        const uint4* xr = reinterpret_cast<const uint4*>(xg + pix * a.x_ld + gsel * (a.C / 2));
-        __nv_bfloat16* yr = yg + pix * a.y_ld + gsel * (a.C / 2);
-        // the residual of the first 32-column block is in flight while the MMA finishes
-        uint4 res[4];
+    bool have = seg_at(t0, t1, PR, &s);
+    int p = have ? s.pa : 0;
+    bool ok = false;
+    const uint4* xr = nullptr;
+    __nv_bfloat16* yr = nullptr;
+    if (have) load_res(2 * s.ip + (int)rank, p, ok, xr, yr);
+    int t = t0;
+    while (have) {
+      // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
+      mbar_wait(&bars[D3FULL], n3 & 1);
+      tc_fence_after();
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) res[q4] = ok ? __ldg(xr + q4) : make_uint4(0, 0, 0, 0);
-        mbar_wait(&bars[D3FULL], n3 & 1);
-        tc_fence_after();
-#pragma unroll 1
-        for (int sub = 0; sub < nsub; ++sub) {
-          const int c0 = sub * 32;
-          uint32_t v[32];
-          tmem_ld32(lanebase + 256 + gsel * (a.C / 2) + c0, v);
-          tmem_wait_ld();
-          if (sub == nsub - 1) {  // D3 drained: the next C3 may overwrite it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) arrive_remote(d3empty_l);
-          }
-          uint4 cur[4];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) cur[q4] = res[q4];
-          if (sub + 1 < nsub) {
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) res[q4] = ok ? __ldg(xr + (sub + 1) * 4 + q4) : make_uint4(0, 0, 0, 0);
-          }
-          if (ok) {
-            uint32_t o[16];
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              const uint32_t uu[4] = {cur[q4].x, cur[q4].y, cur[q4].z, cur[q4].w};
-              const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + c0 + q4 * 8);
-              const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
-              const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const float2 f = unpack_bf16x2(uu[h]);
-                const int c = q4 * 8 + 2 * h;
-                o[q4 * 4 + h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + bb[2 * h] + f.x,
-                                                __uint_as_float(v[c + 1]) + bb[2 * h + 1] + f.y);
-              }
-            }
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4)
-              *reinterpret_cast<uint4*>(yr + c0 + q4 * 8) = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
-          }
+      for (int sub = 0; sub < 4; ++sub) {
+        if (sub >= nsub) break;
+        uint32_t v[32];
+        tmem_ld32(lanebase + 256 + gsel * (a.C / 2) + sub * 32, v);
+        tmem_wait_ld();
+        if (sub == nsub - 1) {  // D3 drained: the next C3 may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_remote(d3empty_l);
         }
-        ++n3;
+        if (ok) {
+          uint32_t o[16];
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            const uint4 u = res[sub * 4 + q4];
+            const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+            const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + sub * 32 + q4 * 8);
+            const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
+            const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float2 f = unpack_bf16x2(uu[h]);
+              const int c = q4 * 8 + 2 * h;
+              o[q4 * 4 + h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + bb[2 * h] + f.x,
+                                              __uint_as_float(v[c + 1]) + bb[2 * h + 1] + f.y);
+            }
+          }
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4)
+            *reinterpret_cast<uint4*>(yr + sub * 32 + q4 * 8) = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
+        }
       }
+      ++n3;
+      // next tile in C3 order; its residual loads are in flight during the next wait
+      if (++p > s.pb) {
+        t += s.pb - s.pa + 1;
+        have = seg_at(t, t1, PR, &s);
+        p = have ? s.pa : 0;
+      }
+      if (have) load_res(2 * s.ip + (int)rank, p, ok, xr, yr);
     }
   }
 
