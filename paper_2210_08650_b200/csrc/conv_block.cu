@@ -84,8 +84,10 @@ enum {
   NBARS = 27
 };
 
-// wait with cluster-scope acquire: the barrier collects arrivals (and the data behind them)
-// from the peer CTA
+// wait on a barrier that collects arrivals from the peer CTA.  CTA-scope acquire: the waiter is
+// the MMA warp, whose reads of the peer's shared memory happen in the async proxy (a
+// cluster-scope acquire compiles to CCTL.IVALL + MEMBAR per poll: measured to stall the
+// whole kernel)
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done = 0, spins = 0;
@@ -99,7 +101,7 @@ __device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t parity) {
     }
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(addr), "r"(parity)
@@ -113,7 +115,10 @@ __device__ __forceinline__ uint32_t mapa_leader(uint32_t local) {
   return r;
 }
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  // (default .release.cta semantics: a cluster-scope release would put a MEMBAR on every arrival;
+  // the data behind these arrivals is consumed by the MMA's async proxy, ordered by the
+  // writers' fence.proxy.async)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA into this CTA's smem, completing on the LEADER's mbarrier (CTA-pair form)
 __device__ __forceinline__ void tma2_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar_leader) {
