@@ -243,6 +243,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
       const int img = 2 * s.ip + (int)rank;  // beyond N: TMA zero fill, stores skipped
       for (int q = s.pa - 1; q <= s.pb + 1; ++q) {
+        // warm L2 with the rows two tiles ahead: the 4-stage ring holds one tile, so the
+        // loads of the next tile have only about one step to arrive
+        if (q + 2 <= s.pb + 1 && elect_one())
+          for (int c = 0; c < kc1; ++c)
+            asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tm_x)), "r"(c * 64), "r"(-1), "r"(2 * (q + 2)), "r"(img)
+                         : "memory");
+        __syncwarp();
         for (int c = 0; c < kc1; ++c) {
           mbar_wait(&bars[XEMPTY + st], ph ^ 1);
           if (elect_one()) {
