@@ -27,6 +27,7 @@
 // columns), 8-11 E1 and E2 (lane quarter w & 3, all 64 columns) -- separate warps so the
 // residual-and-store epilogue of tile p overlaps the t1/t2 epilogues of tiles p+1, p+2 --,
 // 12 TMA producer (weights once, then the x chunks), 13 TMEM allocator + (leader) MMA issuer.
+#include <cstdio>
 #include <cuda_bf16.h>
 
 #include "kernels.h"
@@ -36,6 +37,21 @@ namespace hapi {
 namespace {
 using namespace tcx;
 
+#ifndef BLK_E3_QUAD
+#define BLK_E3_QUAD 0  // 1: E3 moves 16 B chunks quad-coalesced with shfl transposes (A/B)
+#endif
+#ifndef BLK_HINT
+#define BLK_HINT 1  // L2 eviction hints: x evict_last until its residual read, out evict_first
+#endif
+#ifndef BLK_EXP
+#define BLK_EXP 0  // experiment switches for A/B builds only (1 no residual, 2 no store, 4 no x TMA,
+                   // 8 E1 ignores C2DONE, 16 C2 one tap row, 32 print wait cycles)
+#endif
+#if BLK_EXP & 32
+#define PW(i, stmt) do { const long long t_ = clock64(); stmt; pw[i] += clock64() - t_; } while (0)
+#else
+#define PW(i, stmt) stmt
+#endif
 constexpr int B_THREADS = 448;
 constexpr int B_E12_WARP0 = 8;          // warps 8-11: E1 and E2 (one per TMEM lane quarter)
 constexpr int B_PROD_WARP = 12;
@@ -128,11 +144,31 @@ __device__ __forceinline__ void tma2_load_2d(uint32_t dst, const CUtensorMap* ma
       : "memory");
 }
 __device__ __forceinline__ void tma2_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
-                                             uint32_t bar_leader) {
+                                             uint32_t bar_leader, uint64_t policy) {
+#if BLK_HINT
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_leader), "l"(policy)
+      : "memory");
+#else
+  (void)policy;
   asm volatile(
       "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_leader)
       : "memory");
+#endif
+}
+// L2 eviction policies: x stays in L2 between its TMA read (C1) and its residual read (E3),
+// which is its last use; the output streams through
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void mma2(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -150,6 +186,62 @@ __device__ __forceinline__ void commit2(uint64_t* bar) {  // arrive on `bar` in 
 __device__ __forceinline__ uint32_t idesc2(int n) {  // kind::f16, fp32 D, bf16 A/B K-major, M = 256
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
+
+// 256-bit global accesses (one full 32 B sector per lane)
+__device__ __forceinline__ void ldg256(const void* p, uint4& a, uint4& b, uint64_t policy) {
+#if BLK_HINT
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p), "l"(policy));
+#else
+  (void)policy;
+  asm("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+      : "l"(p));
+#endif
+}
+__device__ __forceinline__ void stg256(void* p, const uint4& a, const uint4& b, uint64_t policy) {
+#if BLK_HINT
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p),
+               "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w), "l"(policy)
+               : "memory");
+#else
+  (void)policy;
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+#endif
+}
+// packed fp32x2 add (FADD2), round-to-nearest like two scalar adds
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rc, ra, rb;\n\tmov.b64 {%0, %1}, rc;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
+// 4 x 4 transpose of 16 B chunks inside each lane quad: afterwards lane i of the quad holds in
+// a[j] what lane j held in a[i].  Two stages of 2 x 2 block swaps (shfl.xor 2, then 1).
+__device__ __forceinline__ uint4 shfl_xor4(uint4 v, int m) {
+  return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
+                    __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
+}
+__device__ __forceinline__ void quad_transpose(uint4 (&a)[4], int i) {
+  const bool hi = (i & 2) != 0, od = (i & 1) != 0;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const uint4 r = shfl_xor4(hi ? a[c] : a[c + 2], 2);
+    if (hi) a[c] = r; else a[c + 2] = r;
+  }
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    const uint4 r = shfl_xor4(od ? a[c] : a[c + 1], 1);
+    if (od) a[c] = r; else a[c + 1] = r;
+  }
+}
+__device__ __forceinline__ uint32_t lanebase_of(uint32_t tmem, int quarter) { return tmem + ((uint32_t)(quarter * 32) << 16); }
 
 // Segment schedule: the pair's tile range [t0, t1) over (image pair, row pair) tiles, split at
 // image-pair boundaries.  next_segment() yields (image pair, pa, pb).
@@ -183,6 +275,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
   const int t0 = (int)((long long)T * cl / ncl), t1 = (int)((long long)T * (cl + 1) / ncl);
   const int kc1 = a.C / 64;                     // K chunks of C1
   griddep_launch_dependents();
+#if BLK_EXP & 32
+  unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+#endif
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < B_XS; ++i) {
@@ -238,6 +334,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       tma2_load_2d(sbase + L.w3, &tm_w3, 0, (int)rank * (a.C / 2), wbar);
     }
     __syncwarp();
+    const uint64_t pol_last = policy_evict_last();
     uint32_t st = 0, ph = 0;
     Seg s;
     for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
@@ -245,17 +342,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       for (int q = s.pa - 1; q <= s.pb + 1; ++q) {
         // warm L2 with the rows two tiles ahead: the 4-stage ring holds one tile, so the
         // loads of the next tile have only about one step to arrive
-        if (q + 2 <= s.pb + 1 && elect_one())
+        if (!(BLK_EXP & 4) && q + 2 <= s.pb + 1 && elect_one())
           for (int c = 0; c < kc1; ++c)
+#if BLK_HINT
+            asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.L2::cache_hint [%0, {%1, %2, %3, %4}], %5;" ::"l"(
+                             reinterpret_cast<uint64_t>(&tm_x)), "r"(c * 64), "r"(-1), "r"(2 * (q + 2)), "r"(img), "l"(pol_last)
+                         : "memory");
+#else
             asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(
                              reinterpret_cast<uint64_t>(&tm_x)), "r"(c * 64), "r"(-1), "r"(2 * (q + 2)), "r"(img)
                          : "memory");
+#endif
         __syncwarp();
         for (int c = 0; c < kc1; ++c) {
-          mbar_wait(&bars[XEMPTY + st], ph ^ 1);
-          if (elect_one()) {
+          PW(0, mbar_wait(&bars[XEMPTY + st], ph ^ 1));
+          if (BLK_EXP & 4) {
+            if (rank == 0 && elect_one()) mbar_arrive(&bars[XFULL + st]);
+          } else if (elect_one()) {
             if (rank == 0) mbar_arrive_expect_tx(&bars[XFULL + st], 2u * B_CHUNK);
-            tma2_load_4d(sbase + L.x + st * B_CHUNK, &tm_x, c * 64, -1, 2 * q, img, mapa_leader(lbar(XFULL + st)));
+            tma2_load_4d(sbase + L.x + st * B_CHUNK, &tm_x, c * 64, -1, 2 * q, img, mapa_leader(lbar(XFULL + st)), pol_last);
           }
           __syncwarp();
           if (++st == B_XS) { st = 0; ph ^= 1; }
@@ -275,14 +380,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
         const int n = s.pb - s.pa + 1;
         const int c1b = n1;  // C1 sequence number of this segment's first tile (row pair pa - 1)
         for (int k = 0; k <= n + 3; ++k) {
+          if (k <= n + 1) {
+            // C1(q = pa - 1 + k): x chunks x W1 half -> D1[n1 & 1]
+            const int b = n1 & 1;
+            PW(0, mbar_wait_cl(&bars[D1EMPTY + b], ((n1 >> 1) & 1) ^ 1));
+            tc_fence_after();
+            for (int c = 0; c < kc1; ++c) {
+              PW(1, mbar_wait_cl(&bars[XFULL + st], ph));
+              tc_fence_after();
+              if (elect_one()) {
+                const uint64_t ad = make_sdesc(sbase + L.x + st * B_CHUNK);
+                const uint64_t bd = make_sdesc(sbase + L.w1 + c * 4096);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) mma2(tmem + b * 64, ad + 2 * kk, bd + 2 * kk, id64, (c | kk) != 0);
+                commit2(&bars[XEMPTY + st]);
+                if (c == kc1 - 1) commit2(&bars[D1FULL + b]);
+              }
+              __syncwarp();
+              if (++st == B_XS) { st = 0; ph ^= 1; }
+            }
+            ++n1;
+          }
           if (k >= 3 && k <= n + 2) {
             // C2(p = pa + k - 3): t1 window rows 2p-1 .. 2p+2, written by the E1s of C1 tiles
             // p - 1 .. p + 1 (in order, so waiting for the last suffices)
             const int p = s.pa + k - 3;
             const int need = c1b + (p + 1) - (s.pa - 1);  // sequence number of C1(p + 1), issued last step
-            mbar_wait_cl(&bars[T1READY + (need & 3)], (need >> 2) & 1);
+            PW(2, mbar_wait_cl(&bars[T1READY + (need & 3)], (need >> 2) & 1));
             const int b = n2 & 1;
-            mbar_wait_cl(&bars[D2EMPTY + b], ((n2 >> 1) & 1) ^ 1);
+            PW(3, mbar_wait_cl(&bars[D2EMPTY + b], ((n2 >> 1) & 1) ^ 1));
             tc_fence_after();
             if (elect_one()) {
               const int slot = ((2 * p) % B_SLOTS + B_SLOTS) % B_SLOTS;  // slot of row 2p-1
@@ -291,7 +417,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
               const uint64_t b0 = make_sdesc(sbase + L.w2);
               uint32_t first = 0;
 #pragma unroll 1
-              for (int dr = 0; dr < 3; ++dr) {
+              for (int dr = 0; dr < ((BLK_EXP & 16) ? 1 : 3); ++dr) {
 #pragma unroll
                 for (int dc = 0; dc < 3; ++dc) {
                   // shift (dr * 64 + dc - 1) positions of 128 B = 8 descriptor units each
@@ -311,31 +437,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
             __syncwarp();
             ++n2;
           }
-          if (k <= n + 1) {
-            // C1(q = pa - 1 + k): x chunks x W1 half -> D1[n1 & 1]
-            const int b = n1 & 1;
-            mbar_wait_cl(&bars[D1EMPTY + b], ((n1 >> 1) & 1) ^ 1);
-            tc_fence_after();
-            for (int c = 0; c < kc1; ++c) {
-              mbar_wait_cl(&bars[XFULL + st], ph);
-              tc_fence_after();
-              if (elect_one()) {
-                const uint64_t ad = make_sdesc(sbase + L.x + st * B_CHUNK);
-                const uint64_t bd = make_sdesc(sbase + L.w1 + c * 4096);
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) mma2(tmem + b * 64, ad + 2 * kk, bd + 2 * kk, id64, (c | kk) != 0);
-                commit2(&bars[XEMPTY + st]);
-                if (c == kc1 - 1) commit2(&bars[D1FULL + b]);
-              }
-              __syncwarp();
-              if (++st == B_XS) { st = 0; ph ^= 1; }
-            }
-            ++n1;
-          }
           if (k >= 4) {
             // C3(p = pa + k - 4): t2 x W3 half -> D3
-            mbar_wait_cl(&bars[T2READY], n3 & 1);
-            mbar_wait_cl(&bars[D3EMPTY], (n3 & 1) ^ 1);
+            PW(4, mbar_wait_cl(&bars[T2READY], n3 & 1));
+            PW(5, mbar_wait_cl(&bars[D3EMPTY], (n3 & 1) ^ 1));
             tc_fence_after();
             if (elect_one()) {
               const uint64_t ad = make_sdesc(sbase + L.t2);
@@ -393,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           const int r = 2 * q + ri;
           const bool ok = col_ok && r >= 0 && r < a.H;
           const int b = n1 & 1;
-          mbar_wait(&bars[D1FULL + b], (n1 >> 1) & 1);
+          PW(0, mbar_wait(&bars[D1FULL + b], (n1 >> 1) & 1));
           tc_fence_after();
           uint32_t v0[32], v1[32];
           tmem_ld32(lanebase + b * 64, v0);
@@ -406,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           // segment's last C2.  Wait for the latest C2 issued up to this step.
           {
             const int issued = c2b + (k >= 3 ? ((k < n + 2 ? k : n + 2) - 2) : 0);
-            if (issued > 0) mbar_wait(&bars[C2DONE + ((issued - 1) & 1)], ((issued - 1) >> 1) & 1);
+            if (!(BLK_EXP & 8) && issued > 0) PW(1, mbar_wait(&bars[C2DONE + ((issued - 1) & 1)], ((issued - 1) >> 1) & 1));
           }
           const int slot = ((r + 1) % B_SLOTS + B_SLOTS) % B_SLOTS;
           const uint32_t rowaddr = sbase + L.t1 + slot * B_ROW + pos * 128;
@@ -433,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
         if (k >= 3 && k <= n + 2) {
           // ---- E2(p): relu(D2 + b2) -> t2
           const int b = n2 & 1;
-          mbar_wait(&bars[D2FULL + b], (n2 >> 1) & 1);
+          PW(2, mbar_wait(&bars[D2FULL + b], (n2 >> 1) & 1));
           tc_fence_after();
           uint32_t v0[32], v1[32];
           tmem_ld32(lanebase + 128 + b * 64, v0);
@@ -441,7 +546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           tmem_wait_ld();
           tc_fence_before();
           warp_arrive(d2empty_l + 8u * b);
-          if (n2 >= 1) mbar_wait(&bars[C3DONE], (n2 - 1) & 1);  // C3 of the previous tile read t2
+          if (n2 >= 1) PW(3, mbar_wait(&bars[C3DONE], (n2 - 1) & 1));  // C3 of the previous tile read t2
           const uint32_t rowaddr = sbase + L.t2 + row * 128;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -460,73 +565,101 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       }
     }
   } else if (warp < 8) {
-    // ================================================================ E3 warps
+#if BLK_E3_QUAD
+    // ================================================================ E3 warps (quad-coalesced variant)
+    // Global traffic is quad-coalesced: for one 32-channel block, the four lanes 4g .. 4g+3 of
+    // a quad load / store the 64 contiguous bytes of ONE position per instruction (8 positions
+    // per warp instruction instead of 32 scattered 16 B pieces), and a 4 x 4 transpose of
+    // 16 B chunks inside the quad (two shfl.xor stages) moves each position's chunks to the
+    // lane that owns its TMEM lane.
     const int quarter = warp & 3, gsel = warp >> 2;
-    const int row = quarter * 32 + lane;
-    const int ri = row >> 6, pos = row & 63;
-    const int col = pos - 1;
-    const bool col_ok = col >= 0 && col < a.W;
-    const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
+    const int i4 = lane & 3, g4 = lane & ~3;    // lane within quad, quad's first lane
+    const int ri = quarter >> 1;                // the warp's 32 positions share one tile row
     const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
     const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
     __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
-    const int nsub = a.C / 64;                  // 32-column blocks of this thread's half (<= 4)
-    // the residual of a tile (this thread's C/2 channels, <= 16 x 16 B) is loaded one tile
-    // ahead: its L2 round trip overlaps the wait for the next accumulator
+    const int nsub = a.C / 64;                  // 32-column blocks of this warp's half (<= 4)
+    const int coff = gsel * (a.C / 2) + i4 * 8; // this lane's 16 B chunk within a 32-channel block
+    // position handled by instruction j of this lane: column (quarter & 1) * 32 + g4 + j - 1
+    auto col_of = [&](int j) { return (quarter & 1) * 32 + g4 + j - 1; };
+    // the residual of a tile (C/2 channels of the quad's 4 positions, <= 16 x 16 B) is loaded
+    // one tile ahead: its L2 round trip overlaps the wait for the next accumulator
     uint4 res[16];
-    auto load_res = [&](int img, int p, bool& ok, const uint4*& xr, __nv_bfloat16*& yr) {
+    const __nv_bfloat16* xrow = xg;             // column 0 of the tile row in x / out
+    __nv_bfloat16* yrow = yg;
+    uint32_t okmask = 0;                        // bit j: position of instruction j is stored
+    auto load_res = [&](int img, int p) {
       const int r = 2 * p + ri;
-      ok = img < a.N && col_ok && r < a.H;
-      const long long pix = ((long long)img * a.H + (ok ? r : 0)) * a.W + (ok ? col : 0);
-      xr = reinterpret_cast<const uint4*>(xg + pix * a.x_ld + gsel * (a.C / 2));
-      yr = yg + pix * a.y_ld + gsel * (a.C / 2);
+      const bool rok = img < a.N && r < a.H;
+      const long long rowpix = ((long long)img * a.H + (rok ? r : 0)) * a.W;
+      xrow = xg + rowpix * a.x_ld + coff;
+      yrow = yg + rowpix * a.y_ld + coff;
+      okmask = 0;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) res[j] = (ok && j < nsub * 4) ? __ldg(xr + j) : make_uint4(0, 0, 0, 0);
+      for (int j = 0; j < 4; ++j) {
+        const int c = col_of(j);
+        if (rok && c >= 0 && c < a.W) okmask |= 1u << j;
+      }
+#pragma unroll
+      for (int sub = 0; sub < 4; ++sub)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const bool ld = !(BLK_EXP & 1) && sub < nsub && ((okmask >> j) & 1);
+          res[sub * 4 + j] = ld ? __ldg(reinterpret_cast<const uint4*>(xrow + col_of(j) * a.x_ld + sub * 32))
+                                : make_uint4(0, 0, 0, 0);
+        }
     };
     int n3 = 0;
     Seg s;
     bool have = seg_at(t0, t1, PR, &s);
     int p = have ? s.pa : 0;
-    bool ok = false;
-    const uint4* xr = nullptr;
-    __nv_bfloat16* yr = nullptr;
-    if (have) load_res(2 * s.ip + (int)rank, p, ok, xr, yr);
+    if (have) load_res(2 * s.ip + (int)rank, p);
     int t = t0;
     while (have) {
       // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
-      mbar_wait(&bars[D3FULL], n3 & 1);
+      PW(0, mbar_wait(&bars[D3FULL], n3 & 1));
       tc_fence_after();
 #pragma unroll
       for (int sub = 0; sub < 4; ++sub) {
         if (sub >= nsub) break;
-        uint32_t v[32];
-        tmem_ld32(lanebase + 256 + gsel * (a.C / 2) + sub * 32, v);
-        tmem_wait_ld();
-        if (sub == nsub - 1) {  // D3 drained: the next C3 may overwrite it
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) arrive_remote(d3empty_l);
-        }
-        if (ok) {
-          uint32_t o[16];
+        uint4 rq[4] = {res[sub * 4], res[sub * 4 + 1], res[sub * 4 + 2], res[sub * 4 + 3]};
+        quad_transpose(rq, i4);                 // -> chunk q4 of this lane's own position
+        uint4 oq[4];
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            const uint4 u = res[sub * 4 + q4];
-            const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+        for (int hh = 0; hh < 2; ++hh) {        // 16 accumulator columns at a time (register budget)
+          uint32_t v[16];
+          tmem_ld16(lanebase_of(tmem, quarter) + 256 + gsel * (a.C / 2) + sub * 32 + hh * 16, v);
+          tmem_wait_ld();
+          if (sub == nsub - 1 && hh == 1) {     // D3 drained: the next C3 may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) arrive_remote(d3empty_l);
+          }
+#pragma unroll
+          for (int qq = 0; qq < 2; ++qq) {
+            const int q4 = hh * 2 + qq;
+            const uint32_t uu[4] = {rq[q4].x, rq[q4].y, rq[q4].z, rq[q4].w};
             const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + sub * 32 + q4 * 8);
             const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
             const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            uint32_t o[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
               const float2 f = unpack_bf16x2(uu[h]);
-              const int c = q4 * 8 + 2 * h;
-              o[q4 * 4 + h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + bb[2 * h] + f.x,
-                                              __uint_as_float(v[c + 1]) + bb[2 * h + 1] + f.y);
+              const int c = qq * 8 + 2 * h;
+              o[h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + bb[2 * h] + f.x, __uint_as_float(v[c + 1]) + bb[2 * h + 1] + f.y);
             }
+            oq[q4] = make_uint4(o[0], o[1], o[2], o[3]);
           }
+        }
+        quad_transpose(oq, i4);                 // -> chunk i4 of position g4 + j
+        if (!(BLK_EXP & 2)) {
 #pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4)
-            *reinterpret_cast<uint4*>(yr + sub * 32 + q4 * 8) = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
+          for (int j = 0; j < 4; ++j)
+            if ((okmask >> j) & 1)
+              *reinterpret_cast<uint4*>(yrow + col_of(j) * a.y_ld + sub * 32) = oq[j];
+        } else if (oq[0].x == 0x7fffffffu) {
+          yg[0] = __float2bfloat16(1.f);
         }
       }
       ++n3;
@@ -536,10 +669,109 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
         have = seg_at(t, t1, PR, &s);
         p = have ? s.pa : 0;
       }
-      if (have) load_res(2 * s.ip + (int)rank, p, ok, xr, yr);
+      if (have) load_res(2 * s.ip + (int)rank, p);
     }
+#else
+    // ================================================================ E3 warps
+    // Each lane owns one tile position (its TMEM lane) and moves that position's C/2-channel
+    // half row with 256-bit loads / stores: every access writes or reads a full 32 B sector,
+    // with no data exchange between lanes.
+    const int quarter = warp & 3, gsel = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int ri = row >> 6, pos = row & 63;
+    const int col = pos - 1;
+    const bool col_ok = col >= 0 && col < a.W;
+    const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
+    const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
+    __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
+    const int nsub = a.C / 64;                  // 32-column blocks of this warp's half (<= 4)
+    // the residual of a tile (this thread's C/2 channels, <= 8 x 32 B) is loaded one tile
+    // ahead: its L2 round trip overlaps the wait for the next accumulator
+    uint4 res[16];
+    const uint64_t pol_first = policy_evict_first();
+    bool ok = false;
+    __nv_bfloat16* yr = yg;
+    auto load_res = [&](int img, int p) {
+      const int r = 2 * p + ri;
+      ok = img < a.N && col_ok && r < a.H;
+      const long long pix = ((long long)img * a.H + (ok ? r : 0)) * a.W + (ok ? col : 0);
+      const __nv_bfloat16* xr = xg + pix * a.x_ld + gsel * (a.C / 2);
+      yr = yg + pix * a.y_ld + gsel * (a.C / 2);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (!(BLK_EXP & 1) && ok && j < nsub * 2) ldg256(xr + j * 16, res[2 * j], res[2 * j + 1], pol_first);
+        else res[2 * j] = res[2 * j + 1] = make_uint4(0, 0, 0, 0);
+      }
+    };
+    int n3 = 0;
+    Seg s;
+    bool have = seg_at(t0, t1, PR, &s);
+    int p = have ? s.pa : 0;
+    if (have) load_res(2 * s.ip + (int)rank, p);
+    int t = t0;
+    while (have) {
+      // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
+      PW(0, mbar_wait(&bars[D3FULL], n3 & 1));
+      tc_fence_after();
+      // 16 accumulator columns per step; the TMEM load of step hs + 1 is in flight while
+      // step hs computes and stores
+      const uint32_t d3 = lanebase + 256 + gsel * (a.C / 2);
+      uint32_t va[16], vb[16];
+      tmem_ld16(d3, va);
+      tmem_wait_ld();
+#pragma unroll
+      for (int hs = 0; hs < 8; ++hs) {
+        if (hs >= 2 * nsub) break;
+        uint32_t (&v)[16] = (hs & 1) ? vb : va;
+        uint32_t (&vn)[16] = (hs & 1) ? va : vb;
+        const bool last = hs == 2 * nsub - 1;
+        if (!last) tmem_ld16(d3 + (hs + 1) * 16, vn);
+        uint4 oq[2];
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int q = hs * 2 + qq;            // 8-channel group within the half row
+          const uint4 rr = res[q];
+          const uint32_t uu[4] = {rr.x, rr.y, rr.z, rr.w};
+          const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + q * 8);
+          const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
+          const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const float2 f = unpack_bf16x2(uu[h]);
+            const int c = qq * 8 + 2 * h;
+            const float2 z = add2(add2(make_float2(__uint_as_float(v[c]), __uint_as_float(v[c + 1])),
+                                       make_float2(bb[2 * h], bb[2 * h + 1])), f);
+            o[h] = cvt_relu_bf16x2(z.x, z.y);
+          }
+          oq[qq] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        if (ok && !(BLK_EXP & 2)) stg256(yr + hs * 16, oq[0], oq[1], pol_first);
+        tmem_wait_ld();
+        if (hs == 2 * nsub - 2) {               // D3 fully loaded (the last step's load landed)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) arrive_remote(d3empty_l);
+        }
+      }
+      ++n3;
+      // next tile in C3 order; its residual loads are in flight during the next wait
+      if (++p > s.pb) {
+        t += s.pb - s.pa + 1;
+        have = seg_at(t, t1, PR, &s);
+        p = have ? s.pa : 0;
+      }
+      if (have) load_res(2 * s.ip + (int)rank, p);
+    }
+#endif
   }
 
+#if BLK_EXP & 32
+  if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 4 || warp == 8 || warp == B_PROD_WARP || warp == B_MMA_WARP))
+    printf("blkprof cta %d warp %2d total %lld w0 %llu w1 %llu w2 %llu w3 %llu w4 %llu w5 %llu\n", blockIdx.x, warp,
+           clock64() - t_start, pw[0], pw[1], pw[2], pw[3], pw[4], pw[5]);
+#endif
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();  // no CTA frees TMEM or exits while its peer may still signal it
