@@ -37,15 +37,16 @@ namespace hapi {
 namespace {
 using namespace tcx;
 
-#ifndef BLK_E3_QUAD
-#define BLK_E3_QUAD 0  // 1: E3 moves 16 B chunks quad-coalesced with shfl transposes (A/B)
+#ifndef BLK_UWARP
+#define BLK_UWARP 1  // warp index through shfl: uniform registers, no S2R rematerialization in loops
 #endif
 #ifndef BLK_HINT
 #define BLK_HINT 1  // L2 eviction hints: x evict_last until its residual read, out evict_first
 #endif
 #ifndef BLK_EXP
 #define BLK_EXP 0  // experiment switches for A/B builds only (1 no residual, 2 no store, 4 no x TMA,
-                   // 8 E1 ignores C2DONE, 16 C2 one tap row, 32 print wait cycles)
+                   // 8 E1 ignores C2DONE, 16 C2 one tap row, 32 print wait cycles,
+                   // 64 L2 prefetch of x two tiles ahead (measured: extra DRAM reads), 128 x TMA evict_normal, 256 out evict_normal)
 #endif
 #if BLK_EXP & 32
 #define PW(i, stmt) do { const long long t_ = clock64(); stmt; pw[i] += clock64() - t_; } while (0)
@@ -64,7 +65,7 @@ constexpr int B_SMEM = 232448;
 
 struct BlkLayout {
   // byte offsets from the 1024-aligned base (identical in both CTAs of the pair)
-  int w1, w2, w3, x, t1, t2, bias3, bars, total;
+  int w1, w2, w3, x, t1, t2, bars, total;
   __host__ __device__ static BlkLayout make(int C) {
     BlkLayout L{};
     int o = 0;
@@ -75,7 +76,6 @@ struct BlkLayout {
     o += 1024;                                     // guard before the t1 ring (position -1)
     L.t1 = o; o += (B_SLOTS + 2) * B_ROW + 1024;   // ring + 2 shadows + guard after
     L.t2 = o; o += B_CHUNK;
-    L.bias3 = o; o += C * 4 + 128 * 4;              // b3, then b1 | b2
     L.bars = o; o += 512;
     L.total = o + 1024;                            // + alignment slack
     return L;
@@ -165,6 +165,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -222,26 +227,6 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   return r;
 }
 
-// 4 x 4 transpose of 16 B chunks inside each lane quad: afterwards lane i of the quad holds in
-// a[j] what lane j held in a[i].  Two stages of 2 x 2 block swaps (shfl.xor 2, then 1).
-__device__ __forceinline__ uint4 shfl_xor4(uint4 v, int m) {
-  return make_uint4(__shfl_xor_sync(0xffffffffu, v.x, m), __shfl_xor_sync(0xffffffffu, v.y, m),
-                    __shfl_xor_sync(0xffffffffu, v.z, m), __shfl_xor_sync(0xffffffffu, v.w, m));
-}
-__device__ __forceinline__ void quad_transpose(uint4 (&a)[4], int i) {
-  const bool hi = (i & 2) != 0, od = (i & 1) != 0;
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    const uint4 r = shfl_xor4(hi ? a[c] : a[c + 2], 2);
-    if (hi) a[c] = r; else a[c + 2] = r;
-  }
-#pragma unroll
-  for (int c = 0; c < 4; c += 2) {
-    const uint4 r = shfl_xor4(od ? a[c] : a[c + 1], 1);
-    if (od) a[c] = r; else a[c + 1] = r;
-  }
-}
-__device__ __forceinline__ uint32_t lanebase_of(uint32_t tmem, int quarter) { return tmem + ((uint32_t)(quarter * 32) << 16); }
 
 // Segment schedule: the pair's tile range [t0, t1) over (image pair, row pair) tiles, split at
 // image-pair boundaries.  next_segment() yields (image pair, pa, pb).
@@ -258,16 +243,20 @@ __device__ __forceinline__ bool seg_at(int t, int t1, int PR, Seg* s) {
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
-    conv_block_kernel(const BlockArgs a, const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w1,
+    conv_block_kernel(const __grid_constant__ BlockArgs a, const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w1,
                       const __grid_constant__ CUtensorMap tm_w2, const __grid_constant__ CUtensorMap tm_w3) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const BlkLayout L = BlkLayout::make(a.C);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
-  float* sB3 = reinterpret_cast<float*>(base + L.bias3);
   const uint32_t rank = cluster_ctarank();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#if BLK_UWARP
+  const int warp = __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0);  // warp-uniform: kept in uniform registers
+#else
+  const int warp = threadIdx.x >> 5;
+#endif
+  const int lane = threadIdx.x & 31;
   const int PR = (a.H + 1) / 2;                 // row pairs per image
   const int npairs = (a.N + 1) / 2;             // image pairs
   const int T = npairs * PR;
@@ -305,9 +294,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     *reinterpret_cast<uint4*>(base + L.t1 - 1024 + i * 16) = make_uint4(0, 0, 0, 0);
     *reinterpret_cast<uint4*>(base + L.t1 + (B_SLOTS + 2) * B_ROW + i * 16) = make_uint4(0, 0, 0, 0);
   }
-  for (int i = threadIdx.x; i < a.C; i += B_THREADS) sB3[i] = a.b3 ? __ldg(a.b3 + i) : 0.f;
-  for (int i = threadIdx.x; i < 128; i += B_THREADS)
-    sB3[a.C + i] = i < 64 ? (a.b1 ? __ldg(a.b1 + i) : 0.f) : (a.b2 ? __ldg(a.b2 + i - 64) : 0.f);
   if (warp == B_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
@@ -334,7 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       tma2_load_2d(sbase + L.w3, &tm_w3, 0, (int)rank * (a.C / 2), wbar);
     }
     __syncwarp();
-    const uint64_t pol_last = policy_evict_last();
+    const uint64_t pol_last = (BLK_EXP & 128) ? policy_evict_normal() : policy_evict_last();
     uint32_t st = 0, ph = 0;
     Seg s;
     for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
@@ -342,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       for (int q = s.pa - 1; q <= s.pb + 1; ++q) {
         // warm L2 with the rows two tiles ahead: the 4-stage ring holds one tile, so the
         // loads of the next tile have only about one step to arrive
-        if (!(BLK_EXP & 4) && q + 2 <= s.pb + 1 && elect_one())
+        if ((BLK_EXP & 64) && q + 2 <= s.pb + 1 && elect_one())
           for (int c = 0; c < kc1; ++c)
 #if BLK_HINT
             asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.L2::cache_hint [%0, {%1, %2, %3, %4}], %5;" ::"l"(
@@ -464,26 +450,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     const int col = pos - 1;
     const bool col_ok = col >= 0 && col < a.W;
     const uint32_t lanebase = tmem + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t sb1 = smem_u32(sB3 + a.C), sb2 = sb1 + 64 * 4;
     const uint32_t t1ready_l = mapa_leader(lbar(T1READY));
     const uint32_t t2ready_l = mapa_leader(lbar(T2READY));
     const uint32_t d1empty_l = mapa_leader(lbar(D1EMPTY));
     const uint32_t d2empty_l = mapa_leader(lbar(D2EMPTY));
     auto warp_arrive = [&](uint32_t cluster_bar) {
       __syncwarp();
-      if (lane == 0) arrive_remote(cluster_bar);
+      if (elect_one()) arrive_remote(cluster_bar);
     };
-    // relu(v + bias) of 32 accumulator columns (bias from smem) -> 16 bf16x2
-    auto act32 = [&](const uint32_t (&v)[32], uint32_t bias_addr, bool ok, uint32_t (&o)[16]) {
+    // relu(v + bias) of 32 accumulator columns (bias: kernel parameter, uniform) -> 16 bf16x2
+    auto act32 = [&](const uint32_t (&v)[32], const float* bias, bool ok, uint32_t (&o)[16]) {
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        const float4 q0 = lds_f4(bias_addr + c4 * 32), q1 = lds_f4(bias_addr + c4 * 32 + 16);
-        const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          o[c4 * 4 + j] = ok ? cvt_relu_bf16x2(__uint_as_float(v[c4 * 8 + 2 * j]) + bb[2 * j],
-                                               __uint_as_float(v[c4 * 8 + 2 * j + 1]) + bb[2 * j + 1])
-                             : 0u;
+      for (int j = 0; j < 16; ++j) {
+        const float2 z = add2(make_float2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1])),
+                              make_float2(bias[2 * j], bias[2 * j + 1]));
+        o[j] = ok ? cvt_relu_bf16x2(z.x, z.y) : 0u;
       }
     };
     int n1 = 0, n2 = 0;
@@ -518,7 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t o[16];
-            act32(h ? v1 : v0, sb1 + h * 128, ok, o);
+            act32(h ? v1 : v0, a.b1 + h * 32, ok, o);
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4) {
               const uint32_t off = (((h * 4 + c4) ^ (pos & 7)) << 4);
@@ -551,7 +532,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             uint32_t o[16];
-            act32(h ? v1 : v0, sb2 + h * 128, true, o);
+            act32(h ? v1 : v0, a.b2 + h * 32, true, o);
 #pragma unroll
             for (int c4 = 0; c4 < 4; ++c4)
               asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(rowaddr + (((h * 4 + c4) ^ (row & 7)) << 4)),
@@ -565,118 +546,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       }
     }
   } else if (warp < 8) {
-#if BLK_E3_QUAD
-    // ================================================================ E3 warps (quad-coalesced variant)
-    // Global traffic is quad-coalesced: for one 32-channel block, the four lanes 4g .. 4g+3 of
-    // a quad load / store the 64 contiguous bytes of ONE position per instruction (8 positions
-    // per warp instruction instead of 32 scattered 16 B pieces), and a 4 x 4 transpose of
-    // 16 B chunks inside the quad (two shfl.xor stages) moves each position's chunks to the
-    // lane that owns its TMEM lane.
-    const int quarter = warp & 3, gsel = warp >> 2;
-    const int i4 = lane & 3, g4 = lane & ~3;    // lane within quad, quad's first lane
-    const int ri = quarter >> 1;                // the warp's 32 positions share one tile row
-    const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
-    const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
-    __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
-    const int nsub = a.C / 64;                  // 32-column blocks of this warp's half (<= 4)
-    const int coff = gsel * (a.C / 2) + i4 * 8; // this lane's 16 B chunk within a 32-channel block
-    // position handled by instruction j of this lane: column (quarter & 1) * 32 + g4 + j - 1
-    auto col_of = [&](int j) { return (quarter & 1) * 32 + g4 + j - 1; };
-    // the residual of a tile (C/2 channels of the quad's 4 positions, <= 16 x 16 B) is loaded
-    // one tile ahead: its L2 round trip overlaps the wait for the next accumulator
-    uint4 res[16];
-    const __nv_bfloat16* xrow = xg;             // column 0 of the tile row in x / out
-    __nv_bfloat16* yrow = yg;
-    uint32_t okmask = 0;                        // bit j: position of instruction j is stored
-    auto load_res = [&](int img, int p) {
-      const int r = 2 * p + ri;
-      const bool rok = img < a.N && r < a.H;
-      const long long rowpix = ((long long)img * a.H + (rok ? r : 0)) * a.W;
-      xrow = xg + rowpix * a.x_ld + coff;
-      yrow = yg + rowpix * a.y_ld + coff;
-      okmask = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int c = col_of(j);
-        if (rok && c >= 0 && c < a.W) okmask |= 1u << j;
-      }
-#pragma unroll
-      for (int sub = 0; sub < 4; ++sub)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const bool ld = !(BLK_EXP & 1) && sub < nsub && ((okmask >> j) & 1);
-          res[sub * 4 + j] = ld ? __ldg(reinterpret_cast<const uint4*>(xrow + col_of(j) * a.x_ld + sub * 32))
-                                : make_uint4(0, 0, 0, 0);
-        }
-    };
-    int n3 = 0;
-    Seg s;
-    bool have = seg_at(t0, t1, PR, &s);
-    int p = have ? s.pa : 0;
-    if (have) load_res(2 * s.ip + (int)rank, p);
-    int t = t0;
-    while (have) {
-      // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
-      PW(0, mbar_wait(&bars[D3FULL], n3 & 1));
-      tc_fence_after();
-#pragma unroll
-      for (int sub = 0; sub < 4; ++sub) {
-        if (sub >= nsub) break;
-        uint4 rq[4] = {res[sub * 4], res[sub * 4 + 1], res[sub * 4 + 2], res[sub * 4 + 3]};
-        quad_transpose(rq, i4);                 // -> chunk q4 of this lane's own position
-        uint4 oq[4];
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {        // 16 accumulator columns at a time (register budget)
-          uint32_t v[16];
-          tmem_ld16(lanebase_of(tmem, quarter) + 256 + gsel * (a.C / 2) + sub * 32 + hh * 16, v);
-          tmem_wait_ld();
-          if (sub == nsub - 1 && hh == 1) {     // D3 drained: the next C3 may overwrite it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) arrive_remote(d3empty_l);
-          }
-#pragma unroll
-          for (int qq = 0; qq < 2; ++qq) {
-            const int q4 = hh * 2 + qq;
-            const uint32_t uu[4] = {rq[q4].x, rq[q4].y, rq[q4].z, rq[q4].w};
-            const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + sub * 32 + q4 * 8);
-            const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
-            const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-            uint32_t o[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const float2 f = unpack_bf16x2(uu[h]);
-              const int c = qq * 8 + 2 * h;
-              o[h] = cvt_relu_bf16x2(__uint_as_float(v[c]) + bb[2 * h] + f.x, __uint_as_float(v[c + 1]) + bb[2 * h + 1] + f.y);
-            }
-            oq[q4] = make_uint4(o[0], o[1], o[2], o[3]);
-          }
-        }
-        quad_transpose(oq, i4);                 // -> chunk i4 of position g4 + j
-        if (!(BLK_EXP & 2)) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if ((okmask >> j) & 1)
-              *reinterpret_cast<uint4*>(yrow + col_of(j) * a.y_ld + sub * 32) = oq[j];
-        } else if (oq[0].x == 0x7fffffffu) {
-          yg[0] = __float2bfloat16(1.f);
-        }
-      }
-      ++n3;
-      // next tile in C3 order; its residual loads are in flight during the next wait
-      if (++p > s.pb) {
-        t += s.pb - s.pa + 1;
-        have = seg_at(t, t1, PR, &s);
-        p = have ? s.pa : 0;
-      }
-      if (have) load_res(2 * s.ip + (int)rank, p);
-    }
-#else
     // ================================================================ E3 warps
     // Each lane owns one tile position (its TMEM lane) and moves that position's C/2-channel
     // half row with 256-bit loads / stores: every access writes or reads a full 32 B sector,
     // with no data exchange between lanes.
-    const int quarter = warp & 3, gsel = warp >> 2;
+    const int quarter = warp & 3;
+#if BLK_UWARP
+    const int gsel = warp >> 2;
+#else
+    const int gsel = __shfl_sync(0xffffffffu, warp >> 2, 0);  // warp-uniform (bias reads use uniform registers)
+#endif
     const int row = quarter * 32 + lane;
     const int ri = row >> 6, pos = row & 63;
     const int col = pos - 1;
@@ -687,30 +566,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
     const int nsub = a.C / 64;                  // 32-column blocks of this warp's half (<= 4)
     // the residual of a tile (this thread's C/2 channels, <= 8 x 32 B) is loaded one tile
-    // ahead: its L2 round trip overlaps the wait for the next accumulator
+    // ahead, 32 B at a time: right after step hs of tile p consumed its residual registers,
+    // they are reloaded with tile p+1's, so each L2 round trip overlaps a whole tile
     uint4 res[16];
-    const uint64_t pol_first = policy_evict_first();
-    bool ok = false;
-    __nv_bfloat16* yr = yg;
-    auto load_res = [&](int img, int p) {
-      const int r = 2 * p + ri;
-      ok = img < a.N && col_ok && r < a.H;
-      const long long pix = ((long long)img * a.H + (ok ? r : 0)) * a.W + (ok ? col : 0);
-      const __nv_bfloat16* xr = xg + pix * a.x_ld + gsel * (a.C / 2);
-      yr = yg + pix * a.y_ld + gsel * (a.C / 2);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if (!(BLK_EXP & 1) && ok && j < nsub * 2) ldg256(xr + j * 16, res[2 * j], res[2 * j + 1], pol_first);
-        else res[2 * j] = res[2 * j + 1] = make_uint4(0, 0, 0, 0);
-      }
+    for (int j = 0; j < 16; ++j) res[j] = make_uint4(0, 0, 0, 0);
+    const uint64_t pol_first = policy_evict_first();
+    const uint64_t pol_out = (BLK_EXP & 256) ? policy_evict_normal() : pol_first;
+    auto tile_addr = [&](int img, int p, bool& okk, const __nv_bfloat16*& xr, __nv_bfloat16*& yrr) {
+      const int r = 2 * p + ri;
+      okk = img < a.N && col_ok && r < a.H;
+      const long long pix = ((long long)img * a.H + (okk ? r : 0)) * a.W + (okk ? col : 0);
+      xr = xg + pix * a.x_ld + gsel * (a.C / 2);
+      yrr = yg + pix * a.y_ld + gsel * (a.C / 2);
     };
     int n3 = 0;
     Seg s;
     bool have = seg_at(t0, t1, PR, &s);
     int p = have ? s.pa : 0;
-    if (have) load_res(2 * s.ip + (int)rank, p);
     int t = t0;
+    bool ok = false;
+    const __nv_bfloat16* xr = xg;
+    __nv_bfloat16* yr = yg;
+    if (have) {
+      tile_addr(2 * s.ip + (int)rank, p, ok, xr, yr);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (!(BLK_EXP & 1) && ok && j < nsub * 2) ldg256(xr + j * 16, res[2 * j], res[2 * j + 1], pol_first);
+    }
     while (have) {
+      // the next tile in C3 order
+      Seg sn = s;
+      int pn = p + 1, tn = t;
+      bool have_n = true;
+      if (pn > s.pb) {
+        tn = t + s.pb - s.pa + 1;
+        have_n = seg_at(tn, t1, PR, &sn);
+        pn = have_n ? sn.pa : 0;
+      }
+      bool ok_n = false;
+      const __nv_bfloat16* xr_n = xg;
+      __nv_bfloat16* yr_n = yg;
+      if (have_n) tile_addr(2 * sn.ip + (int)rank, pn, ok_n, xr_n, yr_n);
       // ---- E3(p): relu(D3 + b3 + x) -> out (global, valid positions only)
       PW(0, mbar_wait(&bars[D3FULL], n3 & 1));
       tc_fence_after();
@@ -733,9 +630,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           const int q = hs * 2 + qq;            // 8-channel group within the half row
           const uint4 rr = res[q];
           const uint32_t uu[4] = {rr.x, rr.y, rr.z, rr.w};
-          const uint32_t ba = smem_u32(sB3 + gsel * (a.C / 2) + q * 8);
-          const float4 q0 = lds_f4(ba), q1 = lds_f4(ba + 16);
-          const float bb[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          const float* bb = a.b3 + gsel * (a.C / 2) + q * 8;  // uniform constant-bank operands
           uint32_t o[4];
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
@@ -747,24 +642,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           }
           oq[qq] = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        if (ok && !(BLK_EXP & 2)) stg256(yr + hs * 16, oq[0], oq[1], pol_first);
+        if (!(BLK_EXP & 1) && ok_n) ldg256(xr_n + hs * 16, res[2 * hs], res[2 * hs + 1], pol_first);
+        if (ok && !(BLK_EXP & 2)) stg256(yr + hs * 16, oq[0], oq[1], pol_out);
         tmem_wait_ld();
         if (hs == 2 * nsub - 2) {               // D3 fully loaded (the last step's load landed)
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) arrive_remote(d3empty_l);
+          if (elect_one()) arrive_remote(d3empty_l);
         }
       }
       ++n3;
-      // next tile in C3 order; its residual loads are in flight during the next wait
-      if (++p > s.pb) {
-        t += s.pb - s.pa + 1;
-        have = seg_at(t, t1, PR, &s);
-        p = have ? s.pa : 0;
-      }
-      if (have) load_res(2 * s.ip + (int)rank, p);
+      s = sn;
+      p = pn;
+      t = tn;
+      have = have_n;
+      ok = ok_n;
+      yr = yr_n;
     }
-#endif
   }
 
 #if BLK_EXP & 32

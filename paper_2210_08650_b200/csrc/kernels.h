@@ -148,9 +148,11 @@ struct BlockArgs {
   int N, H, W, C;        // x / y: NHWC [N][H][W][C] bf16
   const void* x; int x_ld;
   void* y; int y_ld;     // must not alias x
-  const float* b1;       // [64]
-  const float* b2;       // [64]
-  const float* b3;       // [C]
+  // folded BN biases BY VALUE (kernel parameter space): every epilogue lane adds the same
+  // bias, which the FADD2s then read as uniform constant-bank operands (no shared loads)
+  float b1[64];
+  float b2[64];
+  float b3[256];         // [C], C <= 256
 };
 struct BlockMaps {
   const CUtensorMap* x;   // 4D {C, W, H, N} over x, box {64, 64, 2, 1}, SW128

@@ -183,6 +183,7 @@ struct ConvW {
   void* w = nullptr;           // bf16 [Cout][Kp] (tc) or fp32 [K][Cout] (simt)
   void* w8 = nullptr;          // s2d stem, mode 8: bf16 [chunk 20][k half 2][n 128][8] (no-swizzle K-major)
   float* bias = nullptr;       // [Cout]
+  std::vector<float> hbias;    // host copy of bias (the block kernel takes it by value)
   float* pro_scale = nullptr;  // [cs]
   float* pro_shift = nullptr;
   CUtensorMap tmap;
@@ -608,6 +609,7 @@ hapi_status make_conv(hapi_model* m, const ConvSpec& s, int* out_idx) {
     cw.w = dw;
   }
   if (has_bias) {
+    cw.hbias = bias;
     hapi_status st = upload(m, bias, &cw.bias);
     if (st != HAPI_OK) return st;
   }
@@ -1471,9 +1473,13 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
       a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = o.in.C;
       a.x = vptr(m, p, o.in, out); a.x_ld = o.in.ld;
       a.y = vptr(m, p, o.out, out); a.y_ld = o.out.ld;
-      a.b1 = m->convs[o.conv].bias;
-      a.b2 = m->convs[o.conv2].bias;
-      a.b3 = m->convs[o.conv3].bias;
+      auto fill = [&](float* dst, int n, const ConvW& cw) {
+        for (int i = 0; i < n; ++i) dst[i] = (int)cw.hbias.size() == n ? cw.hbias[i] : 0.f;
+      };
+      std::memset(a.b3, 0, sizeof(a.b3));
+      fill(a.b1, 64, m->convs[o.conv]);
+      fill(a.b2, 64, m->convs[o.conv2]);
+      fill(a.b3, a.C, m->convs[o.conv3]);
       BlockMaps mp;
       mp.x = &o.bmap_x; mp.w1 = &o.bmap_w1; mp.w2 = &o.bmap_w2; mp.w3 = &o.bmap_w3;
       e = conv_block_launch(a, mp, m->num_sms, st);
