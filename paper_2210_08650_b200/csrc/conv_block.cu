@@ -27,6 +27,12 @@
 // columns), 8-11 E1 and E2 (lane quarter w & 3, all 64 columns) -- separate warps so the
 // residual-and-store epilogue of tile p overlaps the t1/t2 epilogues of tiles p+1, p+2 --,
 // 12 TMA producer (weights once, then the x chunks), 13 TMEM allocator + (leader) MMA issuer.
+//
+// Memory path (DESIGN.md section 10 has the measurements): x is TMA-read with an L2 evict_last
+// policy and re-read as the residual by E3 with evict_first (its last use), so the residual
+// comes from L2; the output streams out with evict_first.  E3 owns one position per lane and
+// moves it with 256-bit loads / stores; the biases are kernel parameters (uniform operands).
+// E3's global accesses are the kernel's limiter (the MMA issuer waits on D3 draining).
 #include <cstdio>
 #include <cuda_bf16.h>
 

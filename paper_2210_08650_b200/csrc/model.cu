@@ -103,10 +103,10 @@ bool stem_pool_enabled() {
   return on;
 }
 
-bool block_enabled() {  // HAPI_BLOCK=1: whole identity bottlenecks on a CTA pair (conv_block.cu)
+bool block_enabled() {  // whole identity bottlenecks on a CTA pair (conv_block.cu); HAPI_BLOCK=0: off
   static const bool on = [] {
     const char* e = std::getenv("HAPI_BLOCK");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   return on;
 }

@@ -73,21 +73,45 @@ def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("arch,split,size,n,flag", [
+    ("resnet50", 21, 96, 6, "HAPI_PAIR"),
+    ("resnet50", 9, 64, 5, "HAPI_PAIR"),
+    ("resnet50", 21, 96, 6, "HAPI_SUB_STORE"),
+])
+def test_stage1_pairs_bitwise_neutral_without_blocks(tmp_path, arch, split, size, n, flag):
+    """With the fused stage-1 blocks off (HAPI_BLOCK=0) the stage-1 conv3 -> conv1 pairs and the
+    layer1 -> layer2 stride-2 store come back; they stay bitwise neutral there too."""
+    fused = _run(tmp_path, {"HAPI_BLOCK": "0"}, arch, split, size, n, "on")
+    plain = _run(tmp_path, {"HAPI_BLOCK": "0", flag: "0"}, arch, split, size, n, "off")
+    assert np.array_equal(fused.view(np.uint32), plain.view(np.uint32)), (flag, int((fused != plain).sum()))
+
+
+@pytest.mark.gpu
 def test_sub_store_is_planned():
     """The layer1 -> layer2 transition pair of ResNet-50 stores its block output at stride 2
     (its only other reader is layer2.0's fused 1x1/s2 downsample); a split at layer1's output
-    (s = 7, the block output is the split layer) keeps the full store."""
-    import paper_2210_08650_b200 as H
-    import hapi_inputs
-    P = list(hapi_inputs.params("resnet50", 1).values())
-    m = H.Model("resnet50", "bf16", P, 2, 7, 21, in_h=96, in_w=96)
-    try:
-        for s in (8, 21):
-            d = m.plan_info(s)["desc"]
-            assert sum("stored at stride 2" in x for x in d) == 1, d
-        assert not any("stored at stride 2" in x for x in m.plan_info(7)["desc"])
-    finally:
-        m.close()
+    (s = 7, the block output is the split layer) keeps the full store.  That pair exists in the
+    layer-at-a-time plan (HAPI_BLOCK=0); the default plan runs layer1.1 and layer1.2 as fused
+    blocks (conv_block.cu), so layer1.2.conv3 is not a pair there."""
+    code = r"""
+import sys
+sys.path.insert(0, %r)
+import paper_2210_08650_b200 as H
+import hapi_inputs
+P = list(hapi_inputs.params("resnet50", 1).values())
+m = H.Model("resnet50", "bf16", P, 2, 7, 21, in_h=96, in_w=96)
+blocked = any(x.startswith("block[") for x in m.plan_info(21)["desc"])
+for s in (8, 21):
+    d = m.plan_info(s)["desc"]
+    assert sum("stored at stride 2" in x for x in d) == (0 if blocked else 1), d
+assert not any("stored at stride 2" in x for x in m.plan_info(7)["desc"])
+m.close()
+print("blocked" if blocked else "plain")
+""" % ROOT
+    for flag, want in (("0", "plain"), ("1", "blocked")):
+        env = dict(os.environ, HAPI_BLOCK=flag)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and r.stdout.strip().endswith(want), r.stderr[-3000:]
 
 
 @pytest.mark.gpu
