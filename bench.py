@@ -208,7 +208,9 @@ def pin_to_gpu_numa_node(local: int):
 def nccl_log_to_stderr():
     """NCCL's INIT lines (version, nRanks, transports) go to stderr, where the driver's log
     capture sees them; stdout stays one JSON line."""
-    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    # the GPU image presets NCCL_DEBUG=VERSION (no INIT lines): raise anything below INFO
+    if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+        os.environ["NCCL_DEBUG"] = "INFO"
     os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
