@@ -1,7 +1,8 @@
 """The fused identity-bottleneck kernel (conv_block.cu: a whole ResNet-50 stage-1 block on a CTA
 pair, t1/t2 on chip, the residual re-read from L2) against the oracle at every split that ends
 inside or after the fused blocks, at 96 px (24x24 stage-1 maps, odd image count: the CTA pair's
-second image is a phantom) and at 224 px (56x56), and against the unfused launches."""
+second image is a phantom), 100 px (25x25: a half-valid last row pair, odd width) and 224 px
+(56x56), and against the unfused launches."""
 import os
 import subprocess
 import sys
@@ -45,7 +46,7 @@ def _run(tmp_path, flag, size, n, splits):
     return np.load(out)
 
 
-@pytest.mark.parametrize("size,n", [(96, 3), (224, 4)])
+@pytest.mark.parametrize("size,n", [(96, 3), (100, 3), (224, 4)])  # 24x24, 25x25 (odd rows / cols), 56x56
 def test_block_kernel_matches_oracle_and_unfused(tmp_path, size, n):
     splits = [5, 6, 7, 8, 21]
     fused = _run(tmp_path, "1", size, n, splits)
