@@ -482,6 +482,25 @@ def main():
                        f"clock, max over ranks; sync_per_step_value = hapi_prefix_forward_host per step",
                "sync_per_step_value": batch * ksteps * world / float(dts[1].item()),
                "host_cores": (f"{len(numa_cores)} cores of the GPU's NUMA node" if numa_cores else "unpinned")}
+        # the same stream of requests with uint8 images (the optional u8 ingest, SURVEY 8(f) f2:
+        # the pack kernel applies x = u / 255 and the rest is the fp32 path), a quarter of the
+        # PCIe H2D bytes; reported beside e2e, not instead of it (the workload's images are fp32)
+        xu = torch.randint(0, 256, tuple(x_host.shape), dtype=torch.uint8,
+                           generator=torch.Generator().manual_seed(seed + rank))
+        xus = [xu.pin_memory(), xu.clone().pin_memory()]
+        model.forward_host_u8(split, xus[0], ohs[0])
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(ksteps):
+            model.forward_host_async_u8(split, xus[i & 1], ohs[i & 1])
+        model.host_sync()
+        du = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(du, op=dist.ReduceOp.MAX)
+        e2e["u8"] = {"value": batch * ksteps * world / float(du.item()), "unit": "img/s",
+                     "h2d_bytes_per_step": int(xu.numel()), "d2h_bytes_per_step": int(out_numel * es),
+                     "note": "hapi_prefix_forward_host_async_u8 per step (uint8 NCHW images, normalised in the "
+                             "input pack kernel), then hapi_host_sync; wall clock, max over ranks"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

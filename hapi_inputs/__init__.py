@@ -6,6 +6,8 @@ selection or size computation).  It only draws random numbers:
 * ``images(n, seed)``: i.i.d. N(0,1) fp32 NCHW 3xHxW tensors -- the paper's
   "random_tensor(input_size)" / "Dataset: Synthetic" (PAPER.md:796, PAPER.md:25;
   reading R6/A10 in DESIGN.md).
+* ``images_u8(n, seed)``: i.i.d. uniform 0..255 uint8 NCHW images (the optional u8
+  ingest of SURVEY 8(f) f2).
 * ``params(arch, seed)``: fp32 weight tensors in torchvision ``state_dict`` order
   (PAPER.md:873 -- the paper used PyTorch; reading A12/A16).  Weights are *data*:
   the same arrays are handed to the oracle (as a name->array dict) and to
@@ -136,6 +138,12 @@ def images(n: int, seed: int, h: int = 224, w: int = 224) -> np.ndarray:
     """fp32 NCHW images, i.i.d. N(0,1), NumPy PCG64."""
     g = np.random.Generator(np.random.PCG64(seed))
     return g.standard_normal((n, 3, h, w), dtype=np.float32)
+
+
+def images_u8(n: int, seed: int, h: int = 224, w: int = 224) -> np.ndarray:
+    """uint8 NCHW images (the u8-ingest calls), i.i.d. uniform over 0..255, NumPy PCG64."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    return g.integers(0, 256, size=(n, 3, h, w), dtype=np.uint8)
 
 
 def params(arch: str, seed: int) -> "OrderedDict[str, np.ndarray]":

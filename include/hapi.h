@@ -294,6 +294,25 @@ HAPI_API hapi_status hapi_prefix_forward_host_async(hapi_model *m, uint32_t spli
 /* Wait for every host-path call enqueued on the model (its copy streams and its stream). */
 HAPI_API hapi_status hapi_host_sync(hapi_model *m);
 
+/* u8 ingest (optional): images arrive as uint8 NCHW [batch,3,in_h,in_w]
+ * (what an image decoder produces; a quarter of the fp32 PCIe bytes of the host path, the
+ * "moving data to and from GPU" overhead of PAPER.md:911) and the input pack kernel turns each
+ * value u of channel c into scale[c] * u + shift[c] in fp32 before the same packing -- the
+ * caller's normalisation (e.g. scale = 1/(255 std), shift = -mean/std) folded into the ingest.
+ * Everything downstream is the fp32 path's (same plans, kernels and fusions).
+ * hapi_model_set_u8_norm: the per-channel scale[3] / shift[3] (host arrays, finite; default
+ * scale 1/255, shift 0); waits for the model's stream, drops the u8 graphs it captured.
+ * hapi_prefix_forward_u8: device images, otherwise as hapi_prefix_forward.
+ * hapi_prefix_forward_host_u8 / _host_async_u8: host images, otherwise as the fp32 host calls.
+ * Errors as the fp32 calls; INVALID_ARGUMENT for a suffix model. */
+HAPI_API hapi_status hapi_model_set_u8_norm(hapi_model *m, const float *scale, const float *shift);
+HAPI_API hapi_status hapi_prefix_forward_u8(hapi_model *m, uint32_t split_idx, const uint8_t *images,
+                                            uint64_t batch, void *out);
+HAPI_API hapi_status hapi_prefix_forward_host_u8(hapi_model *m, uint32_t split_idx, const uint8_t *images,
+                                                 uint64_t batch, void *out);
+HAPI_API hapi_status hapi_prefix_forward_host_async_u8(hapi_model *m, uint32_t split_idx, const uint8_t *images,
+                                                       uint64_t batch, void *out);
+
 /* Device bytes owned by the model: packed weights (+bias/BN vectors), and the activation
  * arena plus the host-path staging (desc.host_chunk) in *arena_bytes. */
 HAPI_API hapi_status hapi_model_device_bytes(const hapi_model *m, uint64_t *weight_bytes, uint64_t *arena_bytes);

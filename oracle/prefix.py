@@ -27,6 +27,19 @@ def prefix_forward(arch: str, params, images: np.ndarray, split_idx: int) -> np.
     return x
 
 
+def normalize_u8(images_u8: np.ndarray, scale, shift) -> np.ndarray:
+    """u8 ingest (optional; the data the client moves to the GPU,
+    PAPER.md:911): uint8 NCHW images become x[n, c] = scale[c] * u[n, c] + shift[c] before
+    layer 1 -- a caller's per-channel normalisation (u / 255 - mean) / std is
+    scale = 1 / (255 std), shift = -mean / std."""
+    u = np.asarray(images_u8)
+    if u.dtype != np.uint8 or u.ndim != 4 or u.shape[1] != 3:
+        raise ValueError("images_u8 must be uint8 [N,3,H,W]")
+    sc = np.asarray(scale, dtype=ops.FLOAT).reshape(1, 3, 1, 1)
+    sh = np.asarray(shift, dtype=ops.FLOAT).reshape(1, 3, 1, 1)
+    return sc * u.astype(ops.FLOAT) + sh
+
+
 def prefix_forward_all(arch: str, params, images: np.ndarray, upto: int | None = None):
     """Outputs of every layer 1..upto (one pass; used by the profiling-run pin)."""
     mods = archs.layers(arch)

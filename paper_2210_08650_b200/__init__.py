@@ -280,10 +280,11 @@ class Model:
         _need(1 <= idx <= len(self.out_bytes), f"layer index {idx} outside [1, {len(self.out_bytes)}]")
         return self.out_bytes[idx - 1]
 
-    def _check_images(self, images, on_device: bool):
+    def _check_images(self, images, on_device: bool, u8: bool = False):
         import torch
         _need(isinstance(images, torch.Tensor), "images must be a torch tensor")
-        _need(images.dtype == torch.float32, f"images must be float32, got {images.dtype}")
+        want = torch.uint8 if u8 else torch.float32
+        _need(images.dtype == want, f"images must be {want}, got {images.dtype}")
         _need(images.dim() == 4 and tuple(images.shape[1:]) == (3, self.in_h, self.in_w),
               f"images must be [N,3,{self.in_h},{self.in_w}], got {tuple(images.shape)}")
         _need(images.is_contiguous(), "images must be contiguous")
@@ -351,6 +352,38 @@ class Model:
 
     def host_sync(self):
         _check(_lib.hapi_host_sync(self._h))
+
+    # u8 ingest: uint8 NCHW images, x = scale[c] * u + shift[c] applied by the input pack kernel
+    def set_u8_norm(self, scale, shift):
+        """Per-channel affine of the u8 calls (3 finite floats each; default 1/255, 0)."""
+        sc = [float(v) for v in scale]
+        sh = [float(v) for v in shift]
+        _need(len(sc) == 3 and len(sh) == 3, "scale and shift take 3 values (one per channel)")
+        _check(_lib.hapi_model_set_u8_norm(self._h, (C.c_float * 3)(*sc), (C.c_float * 3)(*sh)))
+
+    def forward_u8(self, split_idx: int, images, out):
+        """images: CUDA uint8 [batch,3,H,W] contiguous tensor; otherwise as forward()."""
+        self._check_images(images, True, u8=True)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), True)
+        _check(_lib.hapi_prefix_forward_u8(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
+                                           C.c_void_p(out.data_ptr())))
+        return out
+
+    def forward_host_u8(self, split_idx: int, images, out):
+        """Host uint8 images (ideally pinned); synchronous, as forward_host()."""
+        self._check_images(images, False, u8=True)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), False)
+        _check(_lib.hapi_prefix_forward_host_u8(self._h, split_idx, C.c_void_p(images.data_ptr()), images.shape[0],
+                                                C.c_void_p(out.data_ptr())))
+        return out
+
+    def forward_host_async_u8(self, split_idx: int, images, out):
+        """Host uint8 images, enqueued without waiting, as forward_host_async()."""
+        self._check_images(images, False, u8=True)
+        self._check_out(out, images.shape[0] * self._split_bytes(split_idx), False)
+        _check(_lib.hapi_prefix_forward_host_async_u8(self._h, split_idx, C.c_void_p(images.data_ptr()),
+                                                      images.shape[0], C.c_void_p(out.data_ptr())))
+        return out
 
     def forward_timed(self, split_idx: int, images, out) -> List[float]:
         self._check_images(images, True)

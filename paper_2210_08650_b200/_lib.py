@@ -65,6 +65,12 @@ hapi_prefix_forward_host = _sig("hapi_prefix_forward_host", C.c_int, C.c_void_p,
 hapi_prefix_forward_host_async = _sig("hapi_prefix_forward_host_async", C.c_int, C.c_void_p, u32, C.c_void_p, u64,
                                       C.c_void_p)
 hapi_host_sync = _sig("hapi_host_sync", C.c_int, C.c_void_p)
+P_f32 = C.POINTER(C.c_float)
+hapi_model_set_u8_norm = _sig("hapi_model_set_u8_norm", C.c_int, C.c_void_p, P_f32, P_f32)
+hapi_prefix_forward_u8 = _sig("hapi_prefix_forward_u8", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
+hapi_prefix_forward_host_u8 = _sig("hapi_prefix_forward_host_u8", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p)
+hapi_prefix_forward_host_async_u8 = _sig("hapi_prefix_forward_host_async_u8", C.c_int, C.c_void_p, u32, C.c_void_p, u64,
+                                         C.c_void_p)
 hapi_model_device_bytes = _sig("hapi_model_device_bytes", C.c_int, C.c_void_p, P_u64, P_u64)
 hapi_plan_info = _sig("hapi_plan_info", C.c_int, C.c_void_p, u32, P_u32, P_u32, P_dbl, P_dbl, u32)
 hapi_prefix_forward_timed = _sig("hapi_prefix_forward_timed", C.c_int, C.c_void_p, u32, C.c_void_p, u64, C.c_void_p,
@@ -104,4 +110,5 @@ EXPORTED = ["hapi_num_layers", "hapi_freeze_index", "hapi_layer_sizes", "hapi_ch
             "hapi_scheduler_submit", "hapi_scheduler_poll", "hapi_scheduler_finish", "hapi_scheduler_query",
             "hapi_scheduler_destroy", "hapi_model_create_shared", "hapi_server_create", "hapi_server_add_model",
             "hapi_server_submit", "hapi_server_step", "hapi_server_query", "hapi_server_destroy",
-            "hapi_prefix_forward_host_async", "hapi_host_sync"]
+            "hapi_prefix_forward_host_async", "hapi_host_sync", "hapi_model_set_u8_norm", "hapi_prefix_forward_u8",
+            "hapi_prefix_forward_host_u8", "hapi_prefix_forward_host_async_u8"]

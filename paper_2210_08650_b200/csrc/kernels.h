@@ -178,7 +178,13 @@ int conv_simt_ksplit(long long M, int Cout, int K, int num_sms);
 // (channels 3..7 zero).  layout 2: bf16 space-to-depth 2x2 with a zero border ->
 // [N][H/2+3][wp][16] (wp >= W/2+4); padded pixel (i+2, j+3) channel (a*2+b)*3+c holds image pixel
 // (2i+a, 2j+b) channel c; channels 12..15 and the border are zero.
-cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, int wp, cudaStream_t st);
+// u8 ingest: the images arrive as uint8 NCHW and each value becomes
+// scale[c] * u + shift[c] in fp32 before the same packing (fp32 images: nrm == nullptr).
+struct InNorm {
+  float scale[3], shift[3];
+};
+cudaError_t pack_input_launch(const void* img, const InNorm* nrm, void* y, int N, int H, int W, int layout, int wp,
+                              cudaStream_t st);
 // Contiguous NCHW [N][C][HW] (act dtype, es = 2 or 4 bytes) -> NHWC with pixel stride y_ld.
 cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int y_ld, int es, cudaStream_t st);
 

@@ -1,5 +1,5 @@
 // Memory-bound kernels of the hot path:
-//   pack_input   a1: caller NCHW fp32 images -> NHWC activations (bf16 padded to C=4)
+//   pack_input   a1: caller NCHW fp32 (or u8, normalised on the fly) images -> NHWC activations (bf16 padded to C=4)
 //   pool         a4: max 3x3/s2 (-inf padding), max 2x2/s2, avg 2x2/s2 (DenseNet transitions)
 //   adaptive     a4: adaptive / global average pool (ResNet avgpool, DenseNet classifier)
 //   bn_act       a5: unfused eval BN (+ReLU) at split points inside a DenseNet transition,
@@ -62,8 +62,15 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 }
 
 // ---------------------------------------------------------------- pack_input
-__global__ void pack_input_kernel(const float* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout,
-                                  int wp) {
+// one input value: fp32 as is, u8 through the per-channel affine (one FFMA)
+__device__ __forceinline__ float in_val(const float* p, const InNorm&, int) { return __ldg(p); }
+__device__ __forceinline__ float in_val(const uint8_t* p, const InNorm& nrm, int c) {
+  return fmaf((float)__ldg(p), nrm.scale[c], nrm.shift[c]);
+}
+
+template <typename T>
+__global__ void pack_input_kernel(const T* __restrict__ img, void* __restrict__ y, int N, int H, int W, int layout,
+                                  int wp, const InNorm nrm) {
   griddep_launch_dependents();
   griddep_wait();
   const int HW = H * W;
@@ -86,9 +93,9 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
         for (int a = 0; a < 2; ++a)
 #pragma unroll
           for (int b = 0; b < 2; ++b) {
-            const float* src = img + n * 3 * HW + (long long)(2 * i + a) * W + (2 * j + b);
+            const T* src = img + n * 3 * HW + (long long)(2 * i + a) * W + (2 * j + b);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) v[(a * 2 + b) * 3 + c] = __ldg(src + c * HW);
+            for (int c = 0; c < 3; ++c) v[(a * 2 + b) * 3 + c] = in_val(src + c * HW, nrm, c);
           }
       }
       uint4 o0, o1;
@@ -121,9 +128,9 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
           for (int s_ = 0; s_ < 3; ++s_) {
             const int ix = xx + s_ - 1;
             const bool in = iy >= 0 && iy < H && ix >= 0 && ix < W;
-            const float* src = img + n * 3 * HW + (long long)iy * W + ix;
+            const T* src = img + n * 3 * HW + (long long)iy * W + ix;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) v[(r * 3 + s_) * 3 + c] = in ? __ldg(src + c * HW) : 0.f;
+            for (int c = 0; c < 3; ++c) v[(r * 3 + s_) * 3 + c] = in ? in_val(src + c * HW, nrm, c) : 0.f;
           }
         }
         v[27] = 0.f;
@@ -157,9 +164,9 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
       const int i = rem / WP - 1, j = rem - (rem / WP) * WP - 1;
       float v[3] = {0.f, 0.f, 0.f};
       if (i >= 0 && i < H && j >= 0 && j < W) {
-        const float* src = img + n * 3 * HW + (long long)i * W + j;
+        const T* src = img + n * 3 * HW + (long long)i * W + j;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) v[c] = __ldg(src + c * HW);
+        for (int c = 0; c < 3; ++c) v[c] = in_val(src + c * HW, nrm, c);
       }
       uint4 o;
       o.x = pack2(v[0], v[1]); o.y = pack2(v[2], 0.f); o.z = 0u; o.w = 0u;
@@ -171,8 +178,8 @@ __global__ void pack_input_kernel(const float* __restrict__ img, void* __restric
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long n = i / HW;
     const long long p = i - n * HW;
-    const float* src = img + n * 3 * HW + p;
-    const float r = __ldg(src), g = __ldg(src + HW), b = __ldg(src + 2 * HW);
+    const T* src = img + n * 3 * HW + p;
+    const float r = in_val(src, nrm, 0), g = in_val(src + HW, nrm, 1), b = in_val(src + 2 * HW, nrm, 2);
     if (layout == 1) {
       uint4 o;
       o.x = pack2(r, g);
@@ -439,11 +446,18 @@ cudaError_t unpack_nchw_launch(const void* x, int N, int C, int HW, void* y, int
   return cudaGetLastError();
 }
 
-cudaError_t pack_input_launch(const float* img, void* y, int N, int H, int W, int layout, int wp, cudaStream_t st) {
+cudaError_t pack_input_launch(const void* img, const InNorm* nrm, void* y, int N, int H, int W, int layout, int wp,
+                              cudaStream_t st) {
   const long long total = layout == 2 ? (long long)N * (H / 2 + 3) * wp
                           : layout == 3 ? (long long)N * (H + 2) * wp
                           : (long long)N * H * W;
-  launch_pdl(pack_input_kernel, dim3(grid_for(total, 256)), dim3(256), 0, st, img, y, N, H, W, layout, wp);
+  const dim3 grid(grid_for(total, 256)), block(256);
+  if (nrm)
+    launch_pdl(pack_input_kernel<uint8_t>, grid, block, 0, st, static_cast<const uint8_t*>(img), y, N, H, W, layout, wp,
+               *nrm);
+  else
+    launch_pdl(pack_input_kernel<float>, grid, block, 0, st, static_cast<const float*>(img), y, N, H, W, layout, wp,
+               InNorm{});
   return cudaGetLastError();
 }
 

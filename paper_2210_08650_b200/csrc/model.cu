@@ -314,12 +314,15 @@ struct hapi_model {
   struct GraphEntry {
     uint32_t split;
     int nb;
+    bool u8;
     const void* images;
     void* out;
     cudaGraphExec_t exec;
   };
   std::vector<GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;
+  // u8 ingest (hapi_prefix_forward_u8 & co.): x = scale[c] * u + shift[c]
+  InNorm u8norm = {{1.f / 255.f, 1.f / 255.f, 1.f / 255.f}, {0.f, 0.f, 0.f}};
 };
 
 namespace {
@@ -1342,12 +1345,14 @@ inline char* vptr(hapi_model* m, const Plan& p, const View& v, void* ext) {
   return base + (int64_t)v.coff * m->es;
 }
 
-hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const float* images, void* out, cudaStream_t st) {
+hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const void* images, bool in_u8, void* out,
+                      cudaStream_t st) {
   cudaError_t e = cudaSuccess;
   const int isb = m->bf16 ? 1 : 0;
   switch (o.t) {
     case OP_PACK_IN:
-      e = pack_input_launch(images, vptr(m, p, o.out, out), nb, (int)m->d.in_h, (int)m->d.in_w, o.layout, o.out.W, st);
+      e = pack_input_launch(images, in_u8 ? &m->u8norm : nullptr, vptr(m, p, o.out, out), nb, (int)m->d.in_h,
+                            (int)m->d.in_w, o.layout, o.out.W, st);
       break;
     case OP_UNPACK:
       e = unpack_nchw_launch(images, nb, o.out.C, o.out.H * o.out.W, vptr(m, p, o.out, out), o.out.ld, m->es, st);
@@ -1491,11 +1496,11 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const f
   return HAPI_OK;
 }
 
-hapi_status run_chunk(hapi_model* m, const Plan& p, int nb, const float* images, void* out, cudaStream_t st,
+hapi_status run_chunk(hapi_model* m, const Plan& p, int nb, const void* images, bool in_u8, void* out, cudaStream_t st,
                       cudaEvent_t* evs = nullptr) {
   for (size_t k = 0; k < p.ops.size(); ++k) {
     if (evs) cudaEventRecord(evs[k], st);
-    hapi_status s = launch_op(m, p, p.ops[k], nb, images, out, st);
+    hapi_status s = launch_op(m, p, p.ops[k], nb, images, in_u8, out, st);
     if (s != HAPI_OK) return s;
   }
   if (evs) cudaEventRecord(evs[p.ops.size()], st);
@@ -1724,16 +1729,16 @@ bool graphs_enabled() {
 
 // One chunk through the plan, replayed from a cached CUDA graph (captured on first use;
 // PDL attributes become programmatic edges).  Falls back to direct launches if capture fails.
-hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const float* images, void* out) {
-  if (!graphs_enabled()) return run_chunk(m, p, nb, images, out, m->stream);
+hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const void* images, bool in_u8, void* out) {
+  if (!graphs_enabled()) return run_chunk(m, p, nb, images, in_u8, out, m->stream);
   for (auto& g : m->graphs)
-    if (g.split == (uint32_t)p.split && g.nb == nb && g.images == images && g.out == out) {
+    if (g.split == (uint32_t)p.split && g.nb == nb && g.u8 == in_u8 && g.images == images && g.out == out) {
       HAPI_CUDA_TRY(cudaGraphLaunch(g.exec, m->stream));
       return HAPI_OK;
     }
   if (!m->cap_stream) HAPI_CUDA_TRY(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
   HAPI_CUDA_TRY(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
-  hapi_status st = run_chunk(m, p, nb, images, out, m->cap_stream);
+  hapi_status st = run_chunk(m, p, nb, images, in_u8, out, m->cap_stream);
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(m->cap_stream, &graph);
   if (st != HAPI_OK) {
@@ -1745,7 +1750,7 @@ hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const float* i
   // out new pointers): the topology is identical, so update that executable graph's kernel
   // parameters in place instead of instantiating another one.
   for (auto& g : m->graphs) {
-    if (g.split != (uint32_t)p.split || g.nb != nb) continue;
+    if (g.split != (uint32_t)p.split || g.nb != nb || g.u8 != in_u8) continue;
     cudaGraphExecUpdateResultInfo info;
     if (cudaGraphExecUpdate(g.exec, graph, &info) == cudaSuccess) {
       cudaGraphDestroy(graph);
@@ -1765,7 +1770,7 @@ hapi_status run_chunk_graph(hapi_model* m, const Plan& p, int nb, const float* i
     cudaGraphExecDestroy(m->graphs.front().exec);
     m->graphs.erase(m->graphs.begin());
   }
-  m->graphs.push_back({(uint32_t)p.split, nb, images, out, exec});
+  m->graphs.push_back({(uint32_t)p.split, nb, in_u8, images, out, exec});
   HAPI_CUDA_TRY(cudaGraphLaunch(exec, m->stream));
   return HAPI_OK;
 }
@@ -1948,13 +1953,14 @@ hapi_status hapi_suffix_forward(hapi_model* m, uint32_t end_idx, const void* act
     const int nb = (int)std::min<uint64_t>(m->d.max_batch, batch - c0);
     const float* ci = reinterpret_cast<const float*>(static_cast<const char*>(acts) + c0 * m->in_bytes_per_img);
     void* co = static_cast<char*>(out) + c0 * p->out_bytes_per_img;
-    hapi_status st = use_graph ? run_chunk_graph(m, *p, nb, ci, co) : run_chunk(m, *p, nb, ci, co, m->stream);
+    hapi_status st = use_graph ? run_chunk_graph(m, *p, nb, ci, false, co) : run_chunk(m, *p, nb, ci, false, co, m->stream);
     if (st != HAPI_OK) return st;
   }
   return HAPI_OK;
 }
 
-hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
+static hapi_status prefix_forward_impl(hapi_model* m, uint32_t split_idx, const void* images, bool in_u8, uint64_t batch,
+                                       void* out) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
@@ -1963,17 +1969,45 @@ hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* 
   const Plan* p = get_plan(m, split_idx);
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
   HAPI_CUDA_TRY(cudaGetLastError());
-  const int64_t img_elems = 3ll * m->d.in_h * m->d.in_w;
+  const int64_t img_bytes = 3ll * m->d.in_h * m->d.in_w * (in_u8 ? 1 : 4);
   // graphs are keyed by the chunk's pointers: replay them for calls of up to a few chunks,
   // launch directly when a large call would only thrash the cache
   const bool use_graph = (batch + m->d.max_batch - 1) / m->d.max_batch <= 4;
   for (uint64_t c0 = 0; c0 < batch; c0 += m->d.max_batch) {
     const int nb = (int)std::min<uint64_t>(m->d.max_batch, batch - c0);
-    const float* ci = images + c0 * img_elems;
+    const void* ci = static_cast<const char*>(images) + c0 * img_bytes;
     void* co = static_cast<char*>(out) + c0 * p->out_bytes_per_img;
-    hapi_status st = use_graph ? run_chunk_graph(m, *p, nb, ci, co) : run_chunk(m, *p, nb, ci, co, m->stream);
+    hapi_status st = use_graph ? run_chunk_graph(m, *p, nb, ci, in_u8, co) : run_chunk(m, *p, nb, ci, in_u8, co, m->stream);
     if (st != HAPI_OK) return st;
   }
+  return HAPI_OK;
+}
+
+hapi_status hapi_prefix_forward(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
+  return prefix_forward_impl(m, split_idx, images, false, batch, out);
+}
+
+hapi_status hapi_prefix_forward_u8(hapi_model* m, uint32_t split_idx, const uint8_t* images, uint64_t batch, void* out) {
+  return prefix_forward_impl(m, split_idx, images, true, batch, out);
+}
+
+hapi_status hapi_model_set_u8_norm(hapi_model* m, const float* scale, const float* shift) {
+  clear_error();
+  if (!m || !scale || !shift) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
+  for (int c = 0; c < 3; ++c)
+    if (!std::isfinite(scale[c]) || !std::isfinite(shift[c]))
+      return set_error(HAPI_ERR_INVALID_ARGUMENT, "non-finite scale/shift");
+  DeviceGuard dg(m->d.device);
+  // captured graphs hold the old values as kernel parameters: no call may still be replaying them
+  HAPI_CUDA_TRY(cudaStreamSynchronize(m->stream));
+  for (int c = 0; c < 3; ++c) {
+    m->u8norm.scale[c] = scale[c];
+    m->u8norm.shift[c] = shift[c];
+  }
+  for (auto& g : m->graphs)
+    if (g.u8) cudaGraphExecDestroy(g.exec);
+  m->graphs.erase(std::remove_if(m->graphs.begin(), m->graphs.end(), [](const hapi_model::GraphEntry& g) { return g.u8; }),
+                  m->graphs.end());
   return HAPI_OK;
 }
 
@@ -1988,7 +2022,7 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
   if (!p) return set_error(HAPI_ERR_INVALID_ARGUMENT, "split_idx %u outside [%u,%u]", split_idx, m->d.min_split, m->d.max_split);
   std::vector<cudaEvent_t> evs(p->ops.size() + 1);
   for (auto& e : evs) HAPI_CUDA_TRY(cudaEventCreate(&e));
-  hapi_status st = run_chunk(m, *p, (int)batch, images, out, m->stream, evs.data());
+  hapi_status st = run_chunk(m, *p, (int)batch, images, false, out, m->stream, evs.data());
   if (st == HAPI_OK) {
     cudaError_t e = cudaEventSynchronize(evs.back());
     if (e != cudaSuccess) st = set_error(HAPI_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
@@ -1999,11 +2033,11 @@ hapi_status hapi_prefix_forward_timed(hapi_model* m, uint32_t split_idx, const f
   return st;
 }
 
-static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
-                                        void* out, bool ramp_fill);
+static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const void* images, bool in_u8,
+                                        uint64_t batch, void* out, bool ramp_fill);
 
 hapi_status hapi_prefix_forward_host(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch, void* out) {
-  hapi_status st = forward_host_enqueue(m, split_idx, images, batch, out, true);
+  hapi_status st = forward_host_enqueue(m, split_idx, images, false, batch, out, true);
   if (st != HAPI_OK) return st;
   return hapi_host_sync(m);
 }
@@ -2012,7 +2046,19 @@ hapi_status hapi_prefix_forward_host_async(hapi_model* m, uint32_t split_idx, co
                                            void* out) {
   // (no half-size first chunk: in a stream of calls the H2D of this call's first chunk overlaps
   // the previous call's compute, so the fill the ramp shortens is not exposed)
-  return forward_host_enqueue(m, split_idx, images, batch, out, false);
+  return forward_host_enqueue(m, split_idx, images, false, batch, out, false);
+}
+
+hapi_status hapi_prefix_forward_host_u8(hapi_model* m, uint32_t split_idx, const uint8_t* images, uint64_t batch,
+                                        void* out) {
+  hapi_status st = forward_host_enqueue(m, split_idx, images, true, batch, out, true);
+  if (st != HAPI_OK) return st;
+  return hapi_host_sync(m);
+}
+
+hapi_status hapi_prefix_forward_host_async_u8(hapi_model* m, uint32_t split_idx, const uint8_t* images, uint64_t batch,
+                                              void* out) {
+  return forward_host_enqueue(m, split_idx, images, true, batch, out, false);
 }
 
 hapi_status hapi_host_sync(hapi_model* m) {
@@ -2026,8 +2072,8 @@ hapi_status hapi_host_sync(hapi_model* m) {
   return HAPI_OK;
 }
 
-static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const float* images, uint64_t batch,
-                                        void* out, bool ramp_fill) {
+static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const void* images, bool in_u8,
+                                        uint64_t batch, void* out, bool ramp_fill) {
   clear_error();
   if (!m || !images || !out) return set_error(HAPI_ERR_INVALID_ARGUMENT, "null argument");
   if (m->start != 0) return set_error(HAPI_ERR_INVALID_ARGUMENT, "suffix model: use hapi_suffix_forward");
@@ -2037,7 +2083,7 @@ static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const
   if (m->host_chunk == 0)
     return set_error(HAPI_ERR_INVALID_ARGUMENT, "model created with host_chunk = 0 (no host-path staging)");
   DeviceGuard dg(m->d.device);
-  const int64_t img_bytes = 12ll * m->d.in_h * m->d.in_w;
+  const int64_t img_bytes = 3ll * m->d.in_h * m->d.in_w * (in_u8 ? 1 : 4);  // (staging slots are fp32-sized)
   // ev[0..1] h2d done, ev[2..3] compute done, ev[4..5] d2h done (slot reuse)
   cudaStream_t cs = m->stream, xs = m->copy_stream, ys = m->out_stream;
   // sub-chunks so the H2D copy of chunk i+1 and the D2H of chunk i-1 overlap compute of chunk i
@@ -2078,7 +2124,7 @@ static hapi_status forward_host_enqueue(hapi_model* m, uint32_t split_idx, const
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[k], xs));
     HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[k], 0));
     if (gc >= 2) HAPI_CUDA_TRY(cudaStreamWaitEvent(cs, m->ev[4 + k], 0));  // stage_out[k] drained
-    hapi_status st = run_chunk_graph(m, *p, nb, static_cast<const float*>(m->stage_in[k]), m->stage_out[k]);
+    hapi_status st = run_chunk_graph(m, *p, nb, m->stage_in[k], in_u8, m->stage_out[k]);
     if (st != HAPI_OK) return st;
     HAPI_CUDA_TRY(cudaEventRecord(m->ev[2 + k], cs));
     HAPI_CUDA_TRY(cudaStreamWaitEvent(ys, m->ev[2 + k], 0));
