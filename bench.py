@@ -267,6 +267,10 @@ def run_strong(args, wl):
     model.set_stream(stream.cuda_stream)
     gen = torch.Generator(device="cuda").manual_seed(seed * 1000 + rank)
     x = torch.randn(n, 3, 224, 224, generator=gen, device="cuda")
+    # the parity subset (first / last 16 of the shard) comes from the host generator
+    sub_idx, sub = hapi_inputs.parity_subset(seed, a, b)
+    pos = [g - a for g in sub_idx]
+    x[pos] = torch.from_numpy(sub).cuda()
     out = torch.empty(model.out_bytes[split - 1] // 2 * n, dtype=torch.bfloat16, device="cuda")
 
     def barrier():
@@ -297,7 +301,10 @@ def run_strong(args, wl):
             "warmup": max(1, args.warmup // 3), "ms_per_step": tmax * 1e3 / steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": act, "data": "synthetic", "config": config_of(wl, world),
             "clocks": clk.summary(), "e2e": None, "gpu_launches": int(info["n"]) * ((total // world + 511) // 512) * steps,
-            "checksum_ranks": checks}), flush=True)
+            "checksum_ranks": checks, "parity_subset": {"images_per_shard": len(sub_idx),
+                                                        "note": "first/last 16 of each shard drawn on the host "
+                                                                "(hapi_inputs.parity_subset); oracle-checked in "
+                                                                "tests/test_gpu_strong_subset.py"}}), flush=True)
     model.close()
     if world > 1:
         dist.destroy_process_group()

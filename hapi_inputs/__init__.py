@@ -6,6 +6,8 @@ selection or size computation).  It only draws random numbers:
 * ``images(n, seed)``: i.i.d. N(0,1) fp32 NCHW 3xHxW tensors -- the paper's
   "random_tensor(input_size)" / "Dataset: Synthetic" (PAPER.md:796, PAPER.md:25;
   reading R6/A10 in DESIGN.md).
+* ``parity_subset(seed, a, b)``: the first/last 16 images of a shard, host-drawn per global
+  index (the oracle-checked subset of the on-device generated strong-scaling set).
 * ``images_u8(n, seed)``: i.i.d. uniform 0..255 uint8 NCHW images (the optional u8
   ingest of SURVEY 8(f) f2).
 * ``params(arch, seed)``: fp32 weight tensors in torchvision ``state_dict`` order
@@ -138,6 +140,17 @@ def images(n: int, seed: int, h: int = 224, w: int = 224) -> np.ndarray:
     """fp32 NCHW images, i.i.d. N(0,1), NumPy PCG64."""
     g = np.random.Generator(np.random.PCG64(seed))
     return g.standard_normal((n, 3, h, w), dtype=np.float32)
+
+
+def parity_subset(seed: int, a: int, b: int, k: int = 16, h: int = 224, w: int = 224):
+    """The parity subset of the image shard [a, b) of a large generated set (SURVEY 8(d), config
+    5): its first and last k images, each drawn on the host from its own stream keyed by its
+    global index, so the oracle side regenerates exactly what the device run used.
+    -> (global indices, fp32 NCHW array)."""
+    idx = sorted(set(range(a, min(a + k, b))) | set(range(max(b - k, a), b)))
+    arr = np.stack([images(1, 7_000_003 * (seed + 1) + g, h, w)[0] for g in idx]) if idx else \
+        np.zeros((0, 3, h, w), np.float32)
+    return idx, arr
 
 
 def images_u8(n: int, seed: int, h: int = 224, w: int = 224) -> np.ndarray:
