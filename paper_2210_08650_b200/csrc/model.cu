@@ -5,6 +5,7 @@
 // PAPER.md:732; COS batch decoupled from the request, PAPER.md:732/740/750 -> chunking).
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1496,11 +1497,25 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const v
   return HAPI_OK;
 }
 
+// HAPI_NVTX=1: one NVTX range per launch (fused group), named by its plan description -- the
+// per-layer timeline the paper plots in Nsight; with HAPI_GRAPH=0, since a
+// replayed CUDA graph emits no host-side ranges
+bool nvtx_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 hapi_status run_chunk(hapi_model* m, const Plan& p, int nb, const void* images, bool in_u8, void* out, cudaStream_t st,
                       cudaEvent_t* evs = nullptr) {
+  const bool nvtx = nvtx_enabled();
   for (size_t k = 0; k < p.ops.size(); ++k) {
     if (evs) cudaEventRecord(evs[k], st);
+    if (nvtx) nvtxRangePushA(p.ops[k].desc.empty() ? "op" : p.ops[k].desc.c_str());
     hapi_status s = launch_op(m, p, p.ops[k], nb, images, in_u8, out, st);
+    if (nvtx) nvtxRangePop();
     if (s != HAPI_OK) return s;
   }
   if (evs) cudaEventRecord(evs[p.ops.size()], st);

@@ -63,6 +63,7 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("resnet50", 20, 224, 2, "HAPI_NCHW_EPI", None, "0"),   # NCHW epilogue vs NHWC + span pack (7x7)
     ("resnet50", 21, 96, 6, "HAPI_NCHW_EPI", None, "0"),    # ... 3x3 split map
     ("resnet18", 10, 200, 3, "HAPI_NCHW_EPI", None, "0"),   # ... 7x7, 512 channels
+    ("resnet50", 21, 96, 6, "HAPI_NVTX", "1", None),        # NVTX ranges per launch (instrumentation only)
 ])
 def test_fusion_is_bitwise_neutral(tmp_path, arch, split, size, n, flag, on, off):
     fused = _run(tmp_path, {flag: on} if on else {}, arch, split, size, n, "on")
