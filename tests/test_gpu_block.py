@@ -46,7 +46,7 @@ def _run(tmp_path, flag, size, n, splits):
     return np.load(out)
 
 
-@pytest.mark.parametrize("size,n", [(96, 3), (100, 3), (224, 4)])  # 24x24, 25x25 (odd rows / cols), 56x56
+@pytest.mark.parametrize("size,n", [(96, 3), (100, 3), (224, 4), (64, 1)])  # 24x24, 25x25 (odd rows / cols), 56x56, one image
 def test_block_kernel_matches_oracle_and_unfused(tmp_path, size, n):
     splits = [5, 6, 7, 8, 21]
     fused = _run(tmp_path, "1", size, n, splits)

@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_strong_subset.py tests/test_gpu_u8.py -q 2>&1 | tail -3
-timeout 600 python bench.py --workload resnet50_s21_64k --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print(round(d['value']), d['parity_subset'])"
+timeout 900 python -m pytest tests/test_gpu_block.py -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python tools/race_check.py resnet50 21 512 20 2>&1 | tail -3
