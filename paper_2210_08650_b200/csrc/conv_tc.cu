@@ -32,6 +32,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -418,17 +419,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // the next pooled row: V = max(row 2po-1, row 2po, row 2po+1) is the vertical pool, written
     // once to smem for the pooling warps (ReLU >= 0, so padding is 0; max commutes with the
     // bf16 rounding, so V equals pooling the rounded stem map).
-    const int quarter = warp & 3, gsel = warp >> 2;
+    const int quarter = warp & 3;
+    const int gsel = warp >> 2;
     const int row = quarter * 32 + lane;
     const int k = row / g.we, x = row - (row / g.we) * g.we;
     const bool live = k < 2 && x < 2 * g.pq + 1;
-    float bias[32], prev[32];
+    float prev[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int n = gsel * 32 + j;
-      bias[j] = (a.bias && n < a.Cout) ? __ldg(a.bias + n) : 0.f;
-      prev[j] = 0.f;
-    }
+    for (int j = 0; j < 32; ++j) prev[j] = 0.f;
     // a task = (image, strip pair, segment of seg_rows pooled rows); its first tile is the
     // pooled row before the segment (stem rows -2, -1 -- all padding -- for the first segment),
     // whose only use is to leave relu(stem row 2 h0 - 1) in prev for the segment's first row
@@ -454,27 +452,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&pfree[it & 3], ((it >> 2) & 1) ^ 1);
       if (live) {
         const uint32_t dst = smem_u32(sY) + (uint32_t)((it & 3) * (g.ring_bytes / 4) + row * 128);
+        // the channel half is a compile-time constant inside, so the bias parameter reads are
+        // immediate constant-bank operands of the adds
+        auto vpool = [&](auto G) {
+          constexpr int GS = decltype(G)::value;
 #pragma unroll
-        for (int c4 = 0; c4 < 4; ++c4) {
-          uint32_t o[4];
+          for (int c4 = 0; c4 < 4; ++c4) {
+            uint32_t o[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float f[2];
+            for (int j = 0; j < 4; ++j) {
+              float f[2];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              // prev >= 0, so max(prev, a, b) = max(prev, relu(a), relu(b)); padding is -inf
-              const int c = c4 * 8 + 2 * j + h;
-              const float a0 = valid0 ? __uint_as_float(v0[c]) + bias[c] : -INFINITY;
-              const float a1 = valid1 ? __uint_as_float(v1[c]) + bias[c] : -INFINITY;
-              f[h] = fmaxf(fmaxf(prev[c], a0), a1);
-              prev[c] = fmaxf(a1, 0.f);
+              for (int h = 0; h < 2; ++h) {
+                // prev >= 0, so max(prev, a, b) = max(prev, relu(a), relu(b)); padding is -inf
+                const int c = c4 * 8 + 2 * j + h;
+                const float bc = a.bias_u[GS * 32 + c];
+                const float a0 = valid0 ? __uint_as_float(v0[c]) + bc : -INFINITY;
+                const float a1 = valid1 ? __uint_as_float(v1[c]) + bc : -INFINITY;
+                f[h] = fmaxf(fmaxf(prev[c], a0), a1);
+                prev[c] = fmaxf(a1, 0.f);
+              }
+              o[j] = pack_bf16x2(f[0], f[1]);
             }
-            o[j] = pack_bf16x2(f[0], f[1]);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (((GS * 4 + c4) ^ (x & 7)) << 4)),
+                         "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                         : "memory");
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst + (((gsel * 4 + c4) ^ (x & 7)) << 4)),
-                       "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
-                       : "memory");
-        }
+        };
+        if (gsel == 0) vpool(std::integral_constant<int, 0>{});
+        else vpool(std::integral_constant<int, 1>{});
       }
       fence_proxy_async_smem();
       mbar_arrive(&pready[it & 3]);

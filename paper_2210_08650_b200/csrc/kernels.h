@@ -98,6 +98,9 @@ struct ConvArgs {
   // mode 4 with [2 x wb] tiles (wb even, OW % wb == 0, OH even): a 2x2/s2 maxpool follows the
   // conv and is fused into the epilogue; y / y_ld describe the pooled [N][OH/2][OW/2] map
   int pool2;
+  // mode 8 (stem + maxpool, Cout <= 64): the bias BY VALUE, read as uniform constant-bank
+  // operands by the epilogue (a register copy per thread spilled next to its accumulators)
+  float bias_u[64];
 };
 
 // tcgen05 / TMEM / TMA path (bf16 activations, fp32 accumulation).  A-operand modes:

@@ -1397,6 +1397,7 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const v
       a.K = w.K;
       a.w = w.w;
       a.bias = w.bias;
+      for (int i = 0; i < 64; ++i) a.bias_u[i] = i < (int)w.hbias.size() ? w.hbias[i] : 0.f;
       a.pro_scale = w.pro_scale;
       a.pro_shift = w.pro_shift;
       a.res = o.has_res ? vptr(m, p, o.res, out) : nullptr;
