@@ -22,7 +22,7 @@ __device__ __forceinline__ uint64_t desc_none(uint32_t addr, uint32_t lbo, uint3
   return d;
 }
 
-// LA / LB: 0 = SW128, 1 = no swizzle (stem geometry)
+// LA / LB: 0 = SW128, 1 = no swizzle (stem geometry), LA 2 = no swizzle starting one row in
 template <int N, int LA, int LB>
 __global__ void __launch_bounds__(128, 1) mma_lay(int iters, long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -48,14 +48,15 @@ __global__ void __launch_bounds__(128, 1) mma_lay(int iters, long long* out) {
   long long t0 = 0, t1 = 0;
   if (threadIdx.x == 0) {
     // stem geometry: A planes 16 KB apart (LBO), rows 16 B apart; B LBO 2048, SBO 128
-    const uint64_t ad = LA ? desc_none(sa, 16384, 128) : desc_sw128(sa);
+    // LA = 2: the stem's row-shifted view, start 16 B (one 8-channel row) past a 128 B boundary
+    const uint64_t ad = LA == 2 ? desc_none(sa + 16, 16384, 128) : LA ? desc_none(sa, 16384, 128) : desc_sw128(sa);
     const uint64_t bd = LB ? desc_none(sb, 2048, 128) : desc_sw128(sb);
     t0 = clock64();
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
         // SW128: advance 32 B along K inside the atom; no swizzle: shift the start by k rows
-        const uint64_t a = LA ? ad + (k & 7) : ad + 2 * (k & 3);
+        const uint64_t a = LA ? ad + 8 * (k & 3) : ad + 2 * (k & 3);
         const uint64_t b = LB ? bd + 256 * (k & 3) : bd + 2 * (k & 3);
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -101,6 +102,7 @@ int main() {
   report("A noswz,   B noswz (mode-8 stem)", mma_lay<128, 1, 1>, sms, 128);
   report("A noswz,   B SW128", mma_lay<128, 1, 0>, sms, 128);
   report("A SW128,   B noswz", mma_lay<128, 0, 1>, sms, 128);
+  report("A noswz +16 B (row-shifted), B noswz", mma_lay<128, 2, 1>, sms, 128);
   report("A SW128,   B SW128", mma_lay<64, 0, 0>, sms, 64);
   report("A noswz,   B noswz", mma_lay<64, 1, 1>, sms, 64);
   return 0;
