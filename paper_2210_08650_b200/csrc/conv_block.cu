@@ -59,11 +59,12 @@ using namespace tcx;
 #else
 #define PW(i, stmt) stmt
 #endif
-constexpr int B_THREADS = 448;
+constexpr int B_THREADS = 480;
 constexpr int B_E12_WARP0 = 8;          // warps 8-11: E1 and E2 (one per TMEM lane quarter)
 constexpr int B_PROD_WARP = 12;
 constexpr int B_MMA_WARP = 13;
-constexpr int B_XS = 4;                 // x ring stages (one 64-channel chunk of a tile each)
+constexpr int B_XDS_WARP = 14;          // ds blocks: TMA producer of the x tile's second copy (downsample A)
+constexpr int B_XS = 4;                 // x ring stages (one 64-channel chunk of a tile each; ds blocks: 3)
 constexpr int B_SLOTS = 6;              // t1 row slots (+2 shadows)
 constexpr int B_ROW = 64 * 128;         // one t1 row slot: 64 positions x 64 ch bf16
 constexpr int B_CHUNK = 128 * 128;      // one [128 x 64] bf16 operand block (16 KB)
@@ -71,14 +72,17 @@ constexpr int B_SMEM = 232448;
 
 struct BlkLayout {
   // byte offsets from the 1024-aligned base (identical in both CTAs of the pair)
-  int w1, w2, w3, x, t1, t2, bars, total;
-  __host__ __device__ static BlkLayout make(int C) {
+  int w1, w2, w3, wds, x, xds, t1, t2, bars, total, xs;
+  __host__ __device__ static BlkLayout make(int C, int Cout, int ds) {
     BlkLayout L{};
     int o = 0;
     L.w1 = o; o += (C / 64) * (32 * 128);          // W1 half: C/64 chunks of [32 n x 64 k]
     L.w2 = o; o += 9 * (32 * 128);                 // W2 half: 9 taps x [32 x 64]
-    L.w3 = o; o += (C / 2) * 128;                  // W3 half: [C/2 n x 64 k]
-    L.x = o; o += B_XS * B_CHUNK;
+    L.w3 = o; o += (Cout / 2) * 128;               // W3 half: [Cout/2 n x 64 k]
+    L.wds = o; o += ds ? (C / 64) * (Cout / 2) * 128 : 0;  // Wds half: C/64 chunks of [Cout/2 x 64]
+    L.xs = ds ? 3 : B_XS;
+    L.x = o; o += L.xs * B_CHUNK;
+    L.xds = o; o += ds ? B_CHUNK : 0;              // the x tile again, for the downsample MMA
     o += 1024;                                     // guard before the t1 ring (position -1)
     L.t1 = o; o += (B_SLOTS + 2) * B_ROW + 1024;   // ring + 2 shadows + guard after
     L.t2 = o; o += B_CHUNK;
@@ -103,7 +107,9 @@ enum {
   C2DONE = 23,          // [2] each: C2 finished reading the t1 window (commit multicast)
   T2READY = 25,         // leader: E2 written in both CTAs
   C3DONE = 26,          // each: C3 finished reading t2
-  NBARS = 27
+  XDSFULL = 27,         // ds: leader: both CTAs' second x tile landed
+  XDSEMPTY = 28,        // ds: each: the downsample MMA read it (commit multicast)
+  NBARS = 29
 };
 
 // wait on a barrier that collects arrivals from the peer CTA.  CTA-scope acquire: the waiter is
@@ -250,10 +256,11 @@ __device__ __forceinline__ bool seg_at(int t, int t1, int PR, Seg* s) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     conv_block_kernel(const __grid_constant__ BlockArgs a, const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w1,
-                      const __grid_constant__ CUtensorMap tm_w2, const __grid_constant__ CUtensorMap tm_w3) {
+                      const __grid_constant__ CUtensorMap tm_w2, const __grid_constant__ CUtensorMap tm_w3,
+                      const __grid_constant__ CUtensorMap tm_wds) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const BlkLayout L = BlkLayout::make(a.C);
+  const BlkLayout L = BlkLayout::make(a.C, a.Cout, a.ds);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + L.bars);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBARS);
   const uint32_t rank = cluster_ctarank();
@@ -276,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
 #endif
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < B_XS; ++i) {
+    for (int i = 0; i < L.xs; ++i) {
       mbar_init(&bars[XFULL + i], 1);
       mbar_init(&bars[XEMPTY + i], 1);
     }
@@ -293,6 +300,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     for (int i = 0; i < 4; ++i) mbar_init(&bars[T1READY + i], 8);
     mbar_init(&bars[T2READY], 8);
     mbar_init(&bars[C3DONE], 1);
+    mbar_init(&bars[XDSFULL], 1);
+    mbar_init(&bars[XDSEMPTY], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // zero the t1 guards and shadows once (the ring slots are always written before read)
@@ -323,7 +332,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       if (rank == 0) mbar_arrive_expect_tx(&bars[WFULL], 2u * (uint32_t)(L.x - L.w1));
       for (int c = 0; c < kc1; ++c) tma2_load_2d(sbase + L.w1 + c * 4096, &tm_w1, c * 64, (int)rank * 32, wbar);
       for (int t = 0; t < 9; ++t) tma2_load_2d(sbase + L.w2 + t * 4096, &tm_w2, t * 64, (int)rank * 32, wbar);
-      tma2_load_2d(sbase + L.w3, &tm_w3, 0, (int)rank * (a.C / 2), wbar);
+      tma2_load_2d(sbase + L.w3, &tm_w3, 0, (int)rank * (a.Cout / 2), wbar);
+      if (a.ds)
+        for (int c = 0; c < kc1; ++c)
+          tma2_load_2d(sbase + L.wds + c * (a.Cout / 2) * 128, &tm_wds, c * 64, (int)rank * (a.Cout / 2), wbar);
     }
     __syncwarp();
     const uint64_t pol_last = (BLK_EXP & 128) ? policy_evict_normal() : policy_evict_last();
@@ -355,14 +367,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
             tma2_load_4d(sbase + L.x + st * B_CHUNK, &tm_x, c * 64, -1, 2 * q, img, mapa_leader(lbar(XFULL + st)), pol_last);
           }
           __syncwarp();
-          if (++st == B_XS) { st = 0; ph ^= 1; }
+          if (++st == (uint32_t)L.xs) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == B_XDS_WARP) {
+    // ================================================================ ds: second x copy
+    // The downsample MMA of tile p runs with C3(p), three steps after C1(p) consumed x(p) from
+    // the ring, so x(p) is read again (from L2: the ring's TMA loads mark it evict_last) into
+    // one slot, as soon as the previous tile's downsample MMA released it.
+    if (a.ds) {
+      const uint64_t pol_last = policy_evict_last();
+      int n = 0;
+      Seg s;
+      for (int t = t0; seg_at(t, t1, PR, &s); t += s.pb - s.pa + 1) {
+        const int img = 2 * s.ip + (int)rank;
+        for (int p = s.pa; p <= s.pb; ++p, ++n) {
+          mbar_wait(&bars[XDSEMPTY], (n & 1) ^ 1);
+          if (elect_one()) {
+            if (rank == 0) mbar_arrive_expect_tx(&bars[XDSFULL], 2u * (uint32_t)(kc1 * B_CHUNK));
+            for (int c = 0; c < kc1; ++c)
+              tma2_load_4d(sbase + L.xds + c * B_CHUNK, &tm_x, c * 64, -1, 2 * p, img, mapa_leader(lbar(XDSFULL)),
+                           pol_last);
+          }
+          __syncwarp();
         }
       }
     }
   } else if (warp == B_MMA_WARP) {
     // ================================================================ MMA issuer (leader)
     if (rank == 0) {
-      const uint32_t id64 = idesc2(64), id256 = idesc2(a.C);
+      const uint32_t id64 = idesc2(64), id256 = idesc2(a.Cout);
       mbar_wait_cl(&bars[WFULL], 0);
       tc_fence_after();
       uint32_t st = 0, ph = 0;
@@ -389,7 +424,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
                 if (c == kc1 - 1) commit2(&bars[D1FULL + b]);
               }
               __syncwarp();
-              if (++st == B_XS) { st = 0; ph ^= 1; }
+              if (++st == (uint32_t)L.xs) { st = 0; ph ^= 1; }
             }
             ++n1;
           }
@@ -433,6 +468,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
             // C3(p = pa + k - 4): t2 x W3 half -> D3
             PW(4, mbar_wait_cl(&bars[T2READY], n3 & 1));
             PW(5, mbar_wait_cl(&bars[D3EMPTY], (n3 & 1) ^ 1));
+            if (a.ds) mbar_wait_cl(&bars[XDSFULL], n3 & 1);
             tc_fence_after();
             if (elect_one()) {
               const uint64_t ad = make_sdesc(sbase + L.t2);
@@ -440,6 +476,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) mma2(tmem + 256, ad + 2 * kk, bd + 2 * kk, id256, kk != 0);
               commit2(&bars[C3DONE]);
+              if (a.ds) {
+                // the residual is the downsample: D3 += x(p) * Wds over the C input channels,
+                // from the second copy of the x tile
+                for (int c = 0; c < kc1; ++c) {
+                  const uint64_t xd = make_sdesc(sbase + L.xds + c * B_CHUNK);
+                  const uint64_t wd = make_sdesc(sbase + L.wds + c * (a.Cout / 2) * 128);
+#pragma unroll
+                  for (int kk = 0; kk < 4; ++kk) mma2(tmem + 256, xd + 2 * kk, wd + 2 * kk, id256, 1u);
+                }
+                commit2(&bars[XDSEMPTY]);
+              }
               commit2(&bars[D3FULL]);
             }
             __syncwarp();
@@ -570,7 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
     const uint32_t d3empty_l = mapa_leader(lbar(D3EMPTY));
     const __nv_bfloat16* xg = static_cast<const __nv_bfloat16*>(a.x);
     __nv_bfloat16* yg = static_cast<__nv_bfloat16*>(a.y);
-    const int nsub = a.C / 64;                  // 32-column blocks of this warp's half (<= 4)
+    const int nsub = a.Cout / 64;               // 32-column blocks of this warp's half (<= 4)
     // the residual of a tile (this thread's C/2 channels, <= 8 x 32 B) is loaded one tile
     // ahead, 32 B at a time: right after step hs of tile p consumed its residual registers,
     // they are reloaded with tile p+1's, so each L2 round trip overlaps a whole tile
@@ -583,8 +630,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       const int r = 2 * p + ri;
       okk = img < a.N && col_ok && r < a.H;
       const long long pix = ((long long)img * a.H + (okk ? r : 0)) * a.W + (okk ? col : 0);
-      xr = xg + pix * a.x_ld + gsel * (a.C / 2);
-      yrr = yg + pix * a.y_ld + gsel * (a.C / 2);
+      xr = xg + pix * a.x_ld + gsel * (a.Cout / 2);
+      yrr = yg + pix * a.y_ld + gsel * (a.Cout / 2);
     };
     int n3 = 0;
     Seg s;
@@ -598,7 +645,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       tile_addr(2 * s.ip + (int)rank, p, ok, xr, yr);
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (!(BLK_EXP & 1) && ok && j < nsub * 2) ldg256(xr + j * 16, res[2 * j], res[2 * j + 1], pol_first);
+        if (!(BLK_EXP & 1) && !a.ds && ok && j < nsub * 2) ldg256(xr + j * 16, res[2 * j], res[2 * j + 1], pol_first);
     }
     while (have) {
       // the next tile in C3 order
@@ -619,7 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
       tc_fence_after();
       // 16 accumulator columns per step; the TMEM load of step hs + 1 is in flight while
       // step hs computes and stores
-      const uint32_t d3 = lanebase + 256 + gsel * (a.C / 2);
+      const uint32_t d3 = lanebase + 256 + gsel * (a.Cout / 2);
       uint32_t va[16], vb[16];
       tmem_ld16(d3, va);
       tmem_wait_ld();
@@ -636,7 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           const int q = hs * 2 + qq;            // 8-channel group within the half row
           const uint4 rr = res[q];
           const uint32_t uu[4] = {rr.x, rr.y, rr.z, rr.w};
-          const float* bb = a.b3 + gsel * (a.C / 2) + q * 8;  // uniform constant-bank operands
+          const float* bb = a.b3 + gsel * (a.Cout / 2) + q * 8;  // uniform constant-bank operands
           uint32_t o[4];
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
@@ -648,7 +695,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
           }
           oq[qq] = make_uint4(o[0], o[1], o[2], o[3]);
         }
-        if (!(BLK_EXP & 1) && ok_n) ldg256(xr_n + hs * 16, res[2 * hs], res[2 * hs + 1], pol_first);
+        if (!(BLK_EXP & 1) && !a.ds && ok_n) ldg256(xr_n + hs * 16, res[2 * hs], res[2 * hs + 1], pol_first);
         if (ok && !(BLK_EXP & 2)) stg256(yr + hs * 16, oq[0], oq[1], pol_out);
         tmem_wait_ld();
         if (hs == 2 * nsub - 2) {               // D3 fully loaded (the last step's load landed)
@@ -683,12 +730,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(B_THREADS, 1)
 
 }  // namespace
 
-int conv_block_smem_bytes(int C) { return BlkLayout::make(C).total; }
+int conv_block_smem_bytes(int C, int Cout, int ds) { return BlkLayout::make(C, Cout, ds).total; }
 
 cudaError_t conv_block_launch(const BlockArgs& a, const BlockMaps& mp, int num_sms, cudaStream_t st) {
-  if (a.C % 64 != 0 || a.C > 256 || a.W > 62 || a.W < 1 || a.H < 1 || a.N < 1 || !mp.x || !mp.w1 || !mp.w2 || !mp.w3)
+  if (a.C % 64 != 0 || a.C > 256 || a.Cout % 64 != 0 || a.Cout > 256 || a.W > 62 || a.W < 1 || a.H < 1 || a.N < 1 ||
+      !mp.x || !mp.w1 || !mp.w2 || !mp.w3 || (a.ds ? !mp.wds : a.Cout != a.C))
     return cudaErrorInvalidValue;
-  const int smem = BlkLayout::make(a.C).total;
+  const int smem = BlkLayout::make(a.C, a.Cout, a.ds).total;
   if (smem > B_SMEM) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> attr_mask{0};
   {
@@ -709,7 +757,7 @@ cudaError_t conv_block_launch(const BlockArgs& a, const BlockMaps& mp, int num_s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, conv_block_kernel, a, *mp.x, *mp.w1, *mp.w2, *mp.w3);
+  return cudaLaunchKernelEx(&cfg, conv_block_kernel, a, *mp.x, *mp.w1, *mp.w2, *mp.w3, a.ds ? *mp.wds : *mp.w3);
 }
 
 }  // namespace hapi

@@ -148,23 +148,27 @@ cudaError_t conv_pair_launch(const PairArgs& a, const PairMaps& mp, int n2, int 
 // A whole identity bottleneck (1x1 C->64, 3x3 64->64, 1x1 64->C + x, each + folded BN + ReLU) on
 // a CTA pair (conv_block.cu): x is read once, t1/t2 stay on chip.  C <= 256, W <= 62.
 struct BlockArgs {
-  int N, H, W, C;        // x / y: NHWC [N][H][W][C] bf16
+  int N, H, W, C;        // x: NHWC [N][H][W][C] bf16 (C = block input channels)
+  int Cout;              // y: NHWC [N][H][W][Cout]; identity blocks: Cout == C
+  int ds;                // 1: the residual is the block's 1x1/s1 downsample of x (+BN), an MMA
+                         // over a second copy of the x tile (ResNet layer1.0); 0: identity
   const void* x; int x_ld;
   void* y; int y_ld;     // must not alias x
   // folded BN biases BY VALUE (kernel parameter space): every epilogue lane adds the same
   // bias, which the FADD2s then read as uniform constant-bank operands (no shared loads)
   float b1[64];
   float b2[64];
-  float b3[256];         // [C], C <= 256
+  float b3[256];         // [Cout], Cout <= 256 (ds: conv3's and the downsample's biases summed)
 };
 struct BlockMaps {
   const CUtensorMap* x;   // 4D {C, W, H, N} over x, box {64, 64, 2, 1}, SW128
   const CUtensorMap* w1;  // 2D over W1 [64][C], box {64, 32}, SW128
   const CUtensorMap* w2;  // 2D over W2 [64][576] (taps (r, s) x 64 channels), box {64, 32}, SW128
-  const CUtensorMap* w3;  // 2D over W3 [C][64], box {64, C/2}, SW128
+  const CUtensorMap* w3;  // 2D over W3 [Cout][64], box {64, Cout/2}, SW128
+  const CUtensorMap* wds; // ds: 2D over Wds [Cout][C], box {64, Cout/2}, SW128 (else nullptr)
 };
 cudaError_t conv_block_launch(const BlockArgs& a, const BlockMaps& mp, int num_sms, cudaStream_t st);
-int conv_block_smem_bytes(int C);
+int conv_block_smem_bytes(int C, int Cout, int ds);
 
 int conv_tc_pick_bn(int cout);
 int conv_tc_store_cols(int bn);  // columns per epilogue TMA box (64, or bn if smaller)

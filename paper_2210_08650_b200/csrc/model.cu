@@ -112,6 +112,14 @@ bool block_enabled() {  // whole identity bottlenecks on a CTA pair (conv_block.
   return on;
 }
 
+bool block_ds_enabled() {  // HAPI_BLOCK_DS=0: the downsample block (ResNet layer1.0) stays unfused
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_BLOCK_DS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool pair_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_PAIR");
@@ -244,7 +252,8 @@ struct Op {
   // OP_BLOCK (conv_block.cu): conv = conv1, conv2 = conv2, conv3 = conv3 of an identity
   // bottleneck; in = x, out = block output; maps over x and the three weight tensors
   int conv3 = -1;
-  CUtensorMap bmap_x, bmap_w1, bmap_w2, bmap_w3;
+  int conv4 = -1;                // OP_BLOCK with a downsample: its 1x1 conv (else -1)
+  CUtensorMap bmap_x, bmap_w1, bmap_w2, bmap_w3, bmap_wds;
   int in2_stride = 0;            // 0: the conv's own stride2
 };
 
@@ -1032,8 +1041,9 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
         const std::string& p = md.name;
         const int OH = out_dim(cur.H, 3, md.stride, 1), OW = out_dim(cur.W, 3, md.stride, 1);
         View x = cur;
-        if (md.kind == MK_BOTTLENECK && m->bf16 && !md.ds && md.stride == 1 && md.planes == 64 && md.cout == cur.C &&
-            cur.C % 64 == 0 && cur.C <= 256 && cur.W <= 62 && cur.ld == cur.C && cur.coff == 0 && block_enabled()) {
+        if (md.kind == MK_BOTTLENECK && m->bf16 && md.stride == 1 && md.planes == 64 && md.cout % 64 == 0 &&
+            md.cout <= 256 && (md.ds ? block_ds_enabled() : md.cout == cur.C) && cur.C % 64 == 0 && cur.C <= 256 &&
+            cur.W <= 62 && cur.ld == cur.C && cur.coff == 0 && block_enabled()) {
           // the whole block on a CTA pair: x read once (the residual from L2), t1/t2 on chip
           ConvSpec c1, c2, c3;
           c1.wname = p + ".conv1.weight"; c1.fold_bn = p + ".bn1";
@@ -1042,22 +1052,31 @@ hapi_status build_plan(hapi_model* m, int split, Plan* out, bool retarget) {
           c2.cin = 64; c2.cout = 64; c2.k = 3; c2.pad = 1; c2.cs = 64;
           c3.wname = p + ".conv3.weight"; c3.fold_bn = p + ".bn3";
           c3.cin = 64; c3.cout = md.cout; c3.k = 1; c3.cs = 64;
-          int i1, i2, i3;
+          int i1, i2, i3, i4 = -1;
           if ((st = make_conv(m, c1, &i1)) != HAPI_OK || (st = make_conv(m, c2, &i2)) != HAPI_OK ||
               (st = make_conv(m, c3, &i3)) != HAPI_OK)
             return st;
+          if (md.ds) {
+            // ResNet layer1.0: the residual is the 1x1/s1 downsample of x (+BN), an MMA over a
+            // second copy of the x tile inside the same kernel
+            ConvSpec cd;
+            cd.wname = p + ".downsample.0.weight"; cd.fold_bn = p + ".downsample.1";
+            cd.cin = md.cin; cd.cout = md.cout; cd.k = 1; cd.cs = x.C;
+            if ((st = make_conv(m, cd, &i4)) != HAPI_OK) return st;
+          }
           Op o;
           o.t = OP_BLOCK;
           o.in = x;
           o.out = b.compact(md.cout, cur.H, cur.W);
-          o.conv = i1; o.conv2 = i2; o.conv3 = i3;
+          o.conv = i1; o.conv2 = i2; o.conv3 = i3; o.conv4 = i4;
           o.kind = 0;
           const double px = (double)cur.H * cur.W;
-          o.flops = (m->convs[i1].real_flops_per_px + m->convs[i2].real_flops_per_px + m->convs[i3].real_flops_per_px) * px;
-          o.bytes = 2.0 * px * md.cout * m->es;
+          o.flops = (m->convs[i1].real_flops_per_px + m->convs[i2].real_flops_per_px + m->convs[i3].real_flops_per_px +
+                     (i4 >= 0 ? m->convs[i4].real_flops_per_px : 0.0)) * px;
+          o.bytes = px * (x.C + md.cout) * m->es;   // x once (the residual re-read comes from L2) + out
           char d[160];
-          std::snprintf(d, sizeof(d), "block[%s 1x1 C%d->64, 3x3 64->64, 1x1 64->%d +res] %dx%d (CTA pair)", p.c_str(),
-                        x.C, md.cout, cur.H, cur.W);
+          std::snprintf(d, sizeof(d), "block[%s 1x1 C%d->64, 3x3 64->64, 1x1 64->%d %s] %dx%d (CTA pair)", p.c_str(),
+                        x.C, md.cout, md.ds ? "+ds 1x1" : "+res", cur.H, cur.W);
           o.desc = d;
           b.emit(o);
           cur = o.out;
@@ -1478,6 +1497,8 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const v
     case OP_BLOCK: {
       BlockArgs a;
       a.N = nb; a.H = o.in.H; a.W = o.in.W; a.C = o.in.C;
+      a.Cout = o.out.C;
+      a.ds = o.conv4 >= 0 ? 1 : 0;
       a.x = vptr(m, p, o.in, out); a.x_ld = o.in.ld;
       a.y = vptr(m, p, o.out, out); a.y_ld = o.out.ld;
       auto fill = [&](float* dst, int n, const ConvW& cw) {
@@ -1486,9 +1507,14 @@ hapi_status launch_op(hapi_model* m, const Plan& p, const Op& o, int nb, const v
       std::memset(a.b3, 0, sizeof(a.b3));
       fill(a.b1, 64, m->convs[o.conv]);
       fill(a.b2, 64, m->convs[o.conv2]);
-      fill(a.b3, a.C, m->convs[o.conv3]);
+      fill(a.b3, a.Cout, m->convs[o.conv3]);
+      if (a.ds) {  // conv3's and the downsample's folded biases land in the same accumulator
+        const ConvW& wd = m->convs[o.conv4];
+        for (int i = 0; i < a.Cout; ++i) a.b3[i] += (int)wd.hbias.size() == a.Cout ? wd.hbias[i] : 0.f;
+      }
       BlockMaps mp;
       mp.x = &o.bmap_x; mp.w1 = &o.bmap_w1; mp.w2 = &o.bmap_w2; mp.w3 = &o.bmap_w3;
+      mp.wds = o.conv4 >= 0 ? &o.bmap_wds : nullptr;
       e = conv_block_launch(a, mp, m->num_sms, st);
       break;
     }
@@ -1606,6 +1632,7 @@ hapi_status finalize_tmaps(hapi_model* m) {
         if (st == HAPI_OK) st = wmap(&o.bmap_w1, w1, 32);
         if (st == HAPI_OK) st = wmap(&o.bmap_w2, w2, 32);
         if (st == HAPI_OK) st = wmap(&o.bmap_w3, w3, w3.cout / 2);
+        if (st == HAPI_OK && o.conv4 >= 0) st = wmap(&o.bmap_wds, m->convs[o.conv4], m->convs[o.conv4].cout / 2);
         if (st != HAPI_OK) return st;
         continue;
       }

@@ -1,5 +1,6 @@
-"""The fused identity-bottleneck kernel (conv_block.cu: a whole ResNet-50 stage-1 block on a CTA
-pair, t1/t2 on chip, the residual re-read from L2) against the oracle at every split that ends
+"""The fused bottleneck kernel (conv_block.cu: a whole ResNet-50 stage-1 block on a CTA pair, t1/t2
+on chip, the residual re-read from L2, or for layer1.0 the downsample computed from a second copy
+of the x tile) against the oracle at every split that ends
 inside or after the fused blocks, at 96 px (24x24 stage-1 maps, odd image count: the CTA pair's
 second image is a phantom), 100 px (25x25: a half-valid last row pair, odd width) and 224 px
 (56x56), and against the unfused launches."""
@@ -26,6 +27,7 @@ import paper_2210_08650_b200 as H
 m = H.Model(arch, "bf16", list(P.values()), n, 5, 22, in_h=size, in_w=size)
 info = m.plan_info(21)
 assert any(d.startswith("block[") for d in info["desc"]) == {expect_block}, info["desc"]
+assert any("+ds 1x1" in d for d in info["desc"]) == {expect_block}, info["desc"]  # layer1.0, the downsample block
 outs = {{}}
 for s in {splits}:
     y, _ = gpu_forward(arch, "bf16", s, x, P, model=m)
