@@ -740,7 +740,9 @@ cudaError_t conv_block_launch(const BlockArgs& a, const BlockMaps& mp, int num_s
   if (smem > B_SMEM) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> attr_mask{0};
   {
-    cudaError_t e = ensure_smem_attr(attr_mask, conv_block_kernel, smem);
+    // one attribute for every variant: the identity and downsample layouts differ in size, and a
+    // smaller first launch must not leave the attribute too low for a later, larger one
+    cudaError_t e = ensure_smem_attr(attr_mask, conv_block_kernel, B_SMEM);
     if (e != cudaSuccess) return e;
   }
   const long long tiles = (long long)((a.N + 1) / 2) * ((a.H + 1) / 2);

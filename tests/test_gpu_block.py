@@ -57,3 +57,32 @@ def test_block_kernel_matches_oracle_and_unfused(tmp_path, size, n):
         a, b = fused[str(s)], plain[str(s)]
         # same arithmetic up to the fp32 summation order of the residual (epilogue vs in-GEMM)
         assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-2, s
+
+
+_ORDER = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import hapi_inputs
+import paper_2210_08650_b200 as H
+arch, n, size = "resnet50", 2, 96
+P = hapi_inputs.params(arch, 53)
+# a suffix model from layer1.0's output launches the identity blocks first (smaller shared-memory
+# layout); a prefix model then launches the downsample block (larger): both must run
+suf = H.Model(arch, "bf16", list(P.values()), n, 7, 7, in_h=size, in_w=size, start_idx=5)
+a5 = torch.zeros(n * suf.out_bytes[4] // 2, dtype=torch.bfloat16, device="cuda")
+y7 = torch.empty(n * suf.out_bytes[6] // 2, dtype=torch.bfloat16, device="cuda")
+suf.forward_suffix(7, a5.view(n, -1), y7)
+pre = H.Model(arch, "bf16", list(P.values()), n, 5, 5, in_h=size, in_w=size)
+assert any("+ds 1x1" in d for d in pre.plan_info(5)["desc"])
+assert any(d.startswith("block[") for d in suf.plan_info(7)["desc"])
+y5 = torch.empty(n * pre.out_bytes[4] // 2, dtype=torch.bfloat16, device="cuda")
+pre.forward(5, torch.from_numpy(hapi_inputs.images(n, 54, size, size)).cuda(), y5)
+torch.cuda.synchronize()
+assert torch.isfinite(y5.float()).all()
+print("ok")
+"""
+
+
+def test_block_variants_in_either_launch_order():
+    r = subprocess.run([sys.executable, "-c", _ORDER.format(root=ROOT)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
