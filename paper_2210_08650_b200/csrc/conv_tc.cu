@@ -1443,6 +1443,14 @@ bool dual_m256_enabled() {  // HAPI_DUAL_M256=0: im2col convs at BN = 256 with o
   return on;
 }
 
+bool dual_m32_enabled() {  // the halo mode's two M sub-tiles also at BN = 32 (DenseNet 3x3); HAPI_DUAL_M32=0: off
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool dual_m_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("HAPI_DUAL_M");
@@ -1545,12 +1553,13 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
     g.a_stages = 2;
     // two M sub-tiles per B stage (TMEM: 2 buffers x 2 sub-tiles x BN <= 512 columns): halves
     // the weight stream from L2 -- measured -25% on ResNet-50 stage-2 3x3 (BN=128); at BN=64
-    // the MMA is smem-bound and it lost 9%, so BN=128 only, and only if >= 4 B stages still fit
+    // the MMA is smem-bound and it lost 9%, so BN=128 -- and BN=32 (DenseNet's 3x3 128->32: the
+    // 4-row halo box halves the input re-read of the 2-row one, -12%) -- if >= 4 B stages still fit
     {
       const int sb = bn < 64 ? bn : 64;
       const int fixed = 2 * sb * 2 * BM + bn * 4 + 2048;
       const int need = 2 * g.a_stages * g.a_stage_bytes + fixed + 4 * bn * BK * 2;
-      if (bn == 128 && g.n_tiles == 1 && !a.res && need <= SMEM_LIMIT && dual_m_enabled()) g.mt = 2;
+      if ((bn == 128 || (bn == 32 && dual_m32_enabled())) && g.n_tiles == 1 && !a.res && need <= SMEM_LIMIT && dual_m_enabled()) g.mt = 2;
     }
   } else if (mode == 4) {
     if (a.pool2) {
