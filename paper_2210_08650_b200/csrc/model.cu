@@ -704,12 +704,12 @@ struct Builder {
           o.tc_mode = 3;
         } else if (w.stride == 1 && w.kh > 1 && we <= 128 && halo_enabled() &&
                    out.W * ((out.H + ((out.H + 128 / we - 1) / (128 / we)) - 1) / ((out.H + 128 / we - 1) / (128 / we))) >=
-                       (w.bn >= 128 && !res && im2col_enabled() ? 108 : 96)) {
+                       96) {
           // halo mode: one input box per 64-channel block, taps from row-shifted descriptors.
-          // Only when a tile keeps enough of its 128 rows valid: measured on ResNet-50, halo beats
-          // im2col at 116 and 112 valid rows (stage 1 -47%, stage 2 -18%) but loses at 98 (stage 3
-          // 14x14: +10%); narrow-N convs stay on halo (their MMA is smem-bound, and im2col writes
-          // 9x the A bytes into smem), and so do residual convs (ResNet-18 stage 3: 2x slower on im2col)
+          // Only when a tile keeps enough of its 128 rows valid: halo beats im2col at 116 and 112
+          // valid rows (ResNet-50 stage 1 -47%, stage 2 -18%); at 98 (14x14 maps) it was +10% in
+          // round 1 and is now equal on ResNet-50 stage 3 and -2% on the ResNet-18 b200 step, so
+          // the threshold is 96 for every N (it was 108 for wide non-residual convs)
           const int hmax = 128 / we;
           const int tiles_h = (out.H + hmax - 1) / hmax;
           o.hb = (out.H + tiles_h - 1) / tiles_h;
