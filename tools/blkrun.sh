@@ -1,6 +1,3 @@
-timeout 1500 python -m pytest tests/test_gpu_parity.py -q -x 2>&1 | tail -1
-timeout 600 python -m pytest tests/test_gpu_fusion_bits.py -q -x -k "DUAL_M" 2>&1 | tail -1
-for wl in resnet18_s10_b200 resnet50_s21_b512 resnet50_s20_b512; do
-  timeout 300 python tools/layer_profile.py $wl 5 > gpurun_out/halo.txt 2>&1
-  echo "$wl: $(head -1 gpurun_out/halo.txt | cut -c1-80)"
+for i in 1 2; do
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $((29600 + i)) bench.py --gpus 4 --no-cpu-baseline 2> gpurun_out/s4_$i.err | python -c "import json,sys; d=json.loads(sys.stdin.readline()); e=d['e2e']; print(round(d['value']), round(e['value']), round(e['sync_per_step_value']), round(e['u8']['value']), e['host_cores'])"
 done
