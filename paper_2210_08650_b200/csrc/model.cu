@@ -704,12 +704,14 @@ struct Builder {
           o.tc_mode = 3;
         } else if (w.stride == 1 && w.kh > 1 && we <= 128 && halo_enabled() &&
                    out.W * ((out.H + ((out.H + 128 / we - 1) / (128 / we)) - 1) / ((out.H + 128 / we - 1) / (128 / we))) >=
-                       96) {
+                       (w.bn <= 64 ? 64 : 96)) {
           // halo mode: one input box per 64-channel block, taps from row-shifted descriptors.
           // Only when a tile keeps enough of its 128 rows valid: halo beats im2col at 116 and 112
           // valid rows (ResNet-50 stage 1 -47%, stage 2 -18%); at 98 (14x14 maps) it was +10% in
           // round 1 and is now equal on ResNet-50 stage 3 and -2% on the ResNet-18 b200 step, so
-          // the threshold is 96 for every N (it was 108 for wide non-residual convs)
+          // the threshold is 96 (it was 108 for wide non-residual convs).  Narrow-N convs (their
+          // MMA is smem-bound, and im2col writes 9x the A bytes into smem) take halo tiles from 64
+          // valid rows: one 80-column row per tile at 320 px, DenseNet121 s=9 +25%, ResNet-50 +6%
           const int hmax = 128 / we;
           const int tiles_h = (out.H + hmax - 1) / hmax;
           o.hb = (out.H + tiles_h - 1) / tiles_h;
