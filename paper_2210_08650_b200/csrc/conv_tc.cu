@@ -192,7 +192,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   constexpr bool HALO = (MODE == 6 || MODE == 9);
   constexpr bool IM2COL = (MODE == 5 || MODE == 10);
   // MODE 11 = 1x1 mode 3 with two M sub-tiles per weight chunk (g.mode stays 3)
-  constexpr int MT = (MODE == 9 || MODE == 10 || MODE == 11) ? 2 : 1;
+  constexpr int MT = (MODE == 9 || MODE == 10 || MODE == 11 || MODE == 12) ? 2 : 1;
+  constexpr bool PRO = (MODE == 7 || MODE == 12);  // TMA A with the bn-relu prologue in smem (12: two M sub-tiles)
   constexpr bool FLAT = (MODE == 3 || MODE == 11);  // 2D [M][C] TMA tiles
   // TMEM accumulator buffers: two (the epilogue of tile i overlaps the MMAs of tile i+1) unless
   // MT x BN x 2 exceeds the 512 columns -- MODE 10 at BN = 256 keeps one buffer of 2 x 256 columns
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   // epilogue / pooling chain (each pooled row costs that chain more than its 20 MMAs)
   constexpr int NACC = MODE == 8 ? 4 : (MT * BN * 2 <= 512) ? 2 : 1;
   constexpr int TMEM_ALLOC = MODE == 8 ? 512 : NACC == 2 ? C::TMEM_COLS * MT : BN * MT;
-  constexpr bool TMA_A = (FLAT || MODE == 4 || IM2COL || HALO || MODE == 7 || MODE == 8);
+  constexpr bool TMA_A = (FLAT || MODE == 4 || IM2COL || HALO || PRO || MODE == 8);
   constexpr bool SPATIAL = (MODE == 4 || HALO || MODE == 8);
   // 1x1 TMA tiles (mode 3): the epilogue stores per-warp [32 x 32] boxes through the 7th map
   // (tmap_bh, free in mode 3: no multicast there); the CTA-wide staging path is compiled only
@@ -221,8 +222,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint8_t* sR = sY + (MODE == 8 ? g.ring_bytes : 2 * C::SB_BYTES);  // residual ring (if has_res)
   float* sBias = reinterpret_cast<float*>(sR + (g.has_res ? g.res_depth * C::SB_BYTES : 0));
   float* sScale = sBias + BN;                                   // mode 7 prologue tables
-  float* sShift = sScale + (MODE == 7 ? g.pro_c : 0);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sShift + (MODE == 7 ? g.pro_c : 0));
+  float* sShift = sScale + (PRO ? g.pro_c : 0);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sShift + (PRO ? g.pro_c : 0));
   uint64_t* empty = full + MAX_B_STAGES;
   uint64_t* afull = empty + MAX_B_STAGES;    // mode 6 halo ring
   uint64_t* aempty = afull + MAX_A_STAGES;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], MODE == 7 ? NUM_PROD_THREADS : (TMA_A ? 1 : NUM_PROD_THREADS + 1));
+      mbar_init(&full[s], PRO ? NUM_PROD_THREADS : (TMA_A ? 1 : NUM_PROD_THREADS + 1));
       mbar_init(&empty[s], g.mc ? 2 : 1);  // mc: both CTAs' MMAs release the multicast stage
       mbar_init(&lfull[s], 1);
     }
@@ -285,23 +286,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int num_tiles = (g.m_tiles + MT - 1) / MT * g.n_tiles;
   const int OHW = a.OH * a.OW;
 
-  if (MODE == 7 && warp == XFORM_TMA_WARP) {
-    // ================================================================ mode 7 loader
+  if (PRO && warp == XFORM_TMA_WARP) {
+    // ================================================================ mode 7 / 12 loader
     uint32_t stage = 0, phase = 0;
     for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
-      const int tm = tile / g.n_tiles, tn = tile - (tile / g.n_tiles) * g.n_tiles;
+      const int tm = (tile / g.n_tiles) * MT, tn = tile - (tile / g.n_tiles) * g.n_tiles;
       for (int kc = 0; kc < g.k_chunks; ++kc) {
         mbar_wait(&empty[stage], phase ^ 1);
         if (elect_one()) {
-          mbar_arrive_expect_tx(&lfull[stage], g.a_bytes + C::B_STAGE_BYTES);
+          mbar_arrive_expect_tx(&lfull[stage], MT * g.a_bytes + C::B_STAGE_BYTES);
           tma_load_2d(smem_u32(sA + stage * ASZ), &tmap_a, kc * BK, tm * BM, &lfull[stage]);
+          if (MT > 1)  // MODE 12: the second M sub-tile (rows past M read as zeros)
+            tma_load_2d(smem_u32(sA + stage * ASZ + A_STAGE_BYTES), &tmap_a, kc * BK, (tm + 1) * BM, &lfull[stage]);
           tma_load_2d(smem_u32(sB + stage * BSZ), &tmap_b, kc * BK, tn * BN, &lfull[stage]);
         }
         __syncwarp();
         if (++stage == (uint32_t)S) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (MODE == 7 && warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
+  } else if (PRO && warp >= PROD_WARP0 && warp < PROD_WARP0 + 4) {
     // ================================================================ mode 7 transform
     // bn-relu prologue applied in shared memory: thread = tile row, its 8 swizzled 16-byte
     // chunks (conflict-free), channel = chunk ^ (row & 7) inside the 64-channel block
@@ -326,7 +329,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
         const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
         mbar_wait(&lfull[stage], phase);
-        const uint32_t base = smem_u32(sA + stage * ASZ);
+#pragma unroll 1
+        for (int sub = 0; sub < MT; ++sub) {  // MODE 12: both M sub-tiles of the stage
+        const uint32_t base = smem_u32(sA + stage * ASZ) + sub * A_STAGE_BYTES;
         uint32_t w[8][4];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -347,6 +352,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(base + r * 128 + ((j ^ (r & 7)) << 4)),
                        "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
                        : "memory");
+        }
         }
         fence_proxy_async_smem();
         mbar_arrive(&full[stage]);
@@ -1401,7 +1407,12 @@ cudaError_t launch_mode(const ConvArgs& a, const Geo& g, const ConvMaps& mp, int
         return cudaErrorInvalidValue;
       }
       return launch_t<BN, 6>(a, g, mp, num_sms, st);
-    case 7: return launch_t<BN, 7>(a, g, mp, num_sms, st);
+    case 7:
+      if (g.mt == 2) {
+        if constexpr (BN == 128) return launch_t<BN, 12>(a, g, mp, num_sms, st);
+        return cudaErrorInvalidValue;
+      }
+      return launch_t<BN, 7>(a, g, mp, num_sms, st);
     case 8:
       if constexpr (BN == 128) return launch_t<BN, 8>(a, g, mp, num_sms, st);
       return cudaErrorInvalidValue;
@@ -1438,6 +1449,14 @@ bool dual_m1x1_enabled() {  // HAPI_DUAL_M1X1=1: 1x1 convs with two M sub-tiles 
 bool dual_m256_enabled() {  // HAPI_DUAL_M256=0: im2col convs at BN = 256 with one M tile per weight chunk
   static const bool on = [] {
     const char* e = std::getenv("HAPI_DUAL_M256");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool dual_m_pro_enabled() {  // MODE 12 (mode 7 with two M sub-tiles); HAPI_DUAL_M_PRO=0: off
+  static const bool on = [] {
+    const char* e = std::getenv("HAPI_DUAL_M_PRO");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -1602,6 +1621,10 @@ cudaError_t conv_tc_launch(const ConvArgs& a, const ConvMaps& mp, int bn, int mo
   // buffer the short-K tiles wait for every drain), so opt-in: HAPI_DUAL_M1X1=1 (MODE 11)
   if (mode == 3 && (bn == 256 || bn == 128) && !a.res && a.k2_chunks == 0 && a.nchw == 0 && dual_m_enabled() &&
       dual_m1x1_enabled() && (long long)((g.m_tiles + 1) / 2) * g.n_tiles >= 2LL * num_sms)
+    g.mt = 2;
+  // the DenseNet bottleneck 1x1 convs (bn-relu prologue, long K = 64..1000): two M sub-tiles per
+  // weight chunk halve the weight stream from L2 (MODE 12)
+  if (mode == 7 && bn == 128 && g.n_tiles == 1 && !a.res && a.nchw == 0 && dual_m_enabled() && dual_m_pro_enabled())
     g.mt = 2;
   g.k1_chunks = g.k_chunks;
   if (a.k2_chunks > 0) {

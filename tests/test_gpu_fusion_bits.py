@@ -49,6 +49,8 @@ def _run(tmp_path, env_extra, arch, split, size, n, tag):
     ("resnet50", 21, 96, 6, "HAPI_DUAL_M", None, "0"),      # two M sub-tiles per weight stage (halo mode)
     ("densenet121", 9, 64, 5, "HAPI_DUAL_M32", None, "0"),  # ... also at BN = 32 (DenseNet 3x3 128->32)
     ("densenet121", 20, 96, 3, "HAPI_DUAL_M32", None, "0"),
+    ("densenet121", 9, 64, 5, "HAPI_DUAL_M_PRO", None, "0"),  # bn-relu-prologue 1x1 with two M sub-tiles (MODE 12)
+    ("densenet121", 22, 64, 3, "HAPI_DUAL_M_PRO", None, "0"),
     ("resnet50", 21, 224, 3, "HAPI_DUAL_M256", None, "0"),  # ... im2col at BN = 256 (one TMEM buffer), stage 3/4
     ("resnet50", 21, 160, 3, "HAPI_DUAL_M256", None, "0"),  # ... odd M-tile count
     ("resnet50", 21, 224, 401, "HAPI_DUAL_M1X1", "1", None),  # opt-in 1x1 two-M-tile MODE 11 (needs >= 2 waves)
