@@ -1,3 +1,5 @@
-timeout 900 python -m pytest tests/test_gpu_fusion_bits.py -q -k "DUAL_M_PRO or DUAL_M32" 2>&1 | tail -1
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_suffix.py tests/test_gpu_large_inputs.py -q -k "densenet" 2>&1 | tail -1
-timeout 300 python tools/layer_profile.py densenet121_s9_b512 5 2>&1 | head -1
+mkdir -p gpurun_out/ncu
+timeout 300 python tools/prof_step.py vgg11_s21_b256 1 > gpurun_out/ncu/psv.log 2>&1 || exit 1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"conv_tc" --launch-skip 0 --launch-count 1 \
+  -o gpurun_out/ncu/vggstem -f python tools/prof_step.py vgg11_s21_b256 1 > gpurun_out/ncu/vggstem.log 2>&1
+tail -1 gpurun_out/ncu/vggstem.log
