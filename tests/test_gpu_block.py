@@ -84,5 +84,7 @@ print("ok")
 
 
 def test_block_variants_in_either_launch_order():
-    r = subprocess.run([sys.executable, "-c", _ORDER.format(root=ROOT)], capture_output=True, text=True, timeout=600)
+    env = dict(os.environ, HAPI_BLOCK="1", HAPI_BLOCK_DS="1")   # independent of the caller's switches
+    r = subprocess.run([sys.executable, "-c", _ORDER.format(root=ROOT)], env=env, capture_output=True, text=True,
+                       timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
