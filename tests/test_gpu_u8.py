@@ -102,3 +102,27 @@ def test_u8_host_paths_and_norm_change():
             m.set_u8_norm([1.0, 2.0], [0.0, 0.0, 0.0])
     finally:
         m.close()
+
+
+def test_u8_bench_size_sampled():
+    """The u8 ingest at the bench's launch configuration (ResNet50 s=21, batch 512, the
+    fused blocks on): the whole batch bitwise equal to the fp32 path fed the same
+    normalised values, and sampled images checked against the oracle one by one."""
+    import torch
+    import paper_2210_08650_b200 as H
+    arch, act, n, s, sel = "resnet50", "bf16", 512, 21, [0, 1, 510, 511]
+    P = hapi_inputs.params(arch, 65)
+    u8 = hapi_inputs.images_u8(n, 66, 224, 224)
+    m = H.Model(arch, act, list(P.values()), n, s, s)
+    try:
+        m.set_u8_norm(SCALE, SHIFT)
+        a, b = _out(m, s, n, act), _out(m, s, n, act)
+        m.forward_u8(s, torch.from_numpy(u8).cuda(), a)
+        m.forward(s, torch.from_numpy(_fp32_images(u8, SCALE, SHIFT)).cuda(), b)
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+        got = a.float().cpu().numpy().reshape(n, -1)[sel]
+        ref = prefix.prefix_forward(arch, P, prefix.normalize_u8(np.ascontiguousarray(u8[sel]), SCALE, SHIFT), s)
+        check_close(got.reshape(ref.shape), ref, act, "u8 resnet50 s=21 b512 sampled")
+    finally:
+        m.close()
