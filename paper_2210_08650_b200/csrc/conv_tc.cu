@@ -573,9 +573,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     } else if (TMA_A) {
-      if (warp == PROD_WARP0) {
-        uint32_t stage = 0, phase = 0;
-        for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles)) {
+      // mode 4 with one K chunk per tile (the VGG stem): the producer's per-tile work (tile
+      // coordinates: a chain of integer divisions) is longer than the tile's 4 MMAs, so warps
+      // 8-11 each take every 4th tile (tile k_ uses stage k_ mod S, as with one producer)
+      const int np = (MODE == 4 && g.k_chunks == 1 && !g.mc && S > 4) ? 4 : 1;
+      const int pw = warp - PROD_WARP0;
+      if (pw < np) {
+        uint32_t stage = (uint32_t)pw, phase = 0;
+        for (int k_ = pw, tile = tile_at(g, pw, num_tiles); tile >= 0; tile = tile_at(g, k_ += np, num_tiles)) {
           const int tm = (tile / g.n_tiles) * MT, tn = tile - (tile / g.n_tiles) * g.n_tiles;
           // (MT == 1: always one, even for the out-of-range partner tile of an odd multicast pair)
           const int nsub = MT == 1 ? 1 : (g.m_tiles - tm < MT ? g.m_tiles - tm : MT);
@@ -670,6 +675,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (++sft == a.KW) { sft = 0; ++r; }
               }
             }
+          }
+          if (np > 1) {  // skip the other producers' stages (np < S: at most one wrap)
+            stage += (uint32_t)(np - 1);
+            if (stage >= (uint32_t)S) { stage -= (uint32_t)S; phase ^= 1; }
           }
         }
       }
