@@ -993,13 +993,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t stg = smem_u32(sY + grp * C::SB_BYTES);
       const int pq = g.wb >> 1, nchunk = BN / 8, PW = a.OW >> 1;
       __nv_bfloat16* yp = static_cast<__nv_bfloat16*>(a.y);
-      for (int k_ = 0, tile = tile_at(g, 0, num_tiles); tile >= 0; tile = tile_at(g, ++k_, num_tiles), ++iter) {
-        const int acc = iter & 1;
-        if (acc != grp) continue;
-        mbar_wait(&tfull[acc], (iter >> 1) & 1);
+      // the group's tiles are k_ = grp, grp + 2, ...: without multicast (one N tile) the tile index
+      // advances by 2 x gridDim.x, so its coordinates are carried forward instead of re-divided
+      const bool inc = !g.mc && g.n_tiles == 1;
+      const int TW = g.tiles_w, TH = g.tiles_h, D = 2 * (int)gridDim.x;
+      const int dw = D % TW, dh = (D / TW) % TH, db = D / (TW * TH);
+      int tw = 0, th = 0, tb = 0;
+      for (int k_ = grp, tile = tile_at(g, grp, num_tiles); tile >= 0; tile = tile_at(g, k_ += 2, num_tiles)) {
+        const int acc = grp;  // == k_ & 1
+        mbar_wait(&tfull[acc], (k_ >> 1) & 1);
         tc_fence_after();
         int w0 = 0, h0 = 0, b0 = 0;
-        tile_origin(g, tile / g.n_tiles, &w0, &h0, &b0);
+        if (!inc) {
+          tile_origin(g, tile / g.n_tiles, &w0, &h0, &b0);
+        } else {
+          if (k_ == grp) {
+            tw = tile % TW; th = (tile / TW) % TH; tb = tile / (TW * TH);
+          } else {
+            tw += dw;
+            int c = tw >= TW ? 1 : 0;
+            tw -= c * TW;
+            th += dh + c;
+            c = th >= TH ? 1 : 0;
+            th -= c * TH;
+            tb += db + c;
+          }
+          w0 = tw * g.wb; h0 = th * g.hb; b0 = tb * g.nb;
+        }
         const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
 #pragma unroll
         for (int sub = 0; sub < BN / 32; ++sub) {

@@ -1,4 +1,4 @@
-# A/B: VGG11 stem epilogue: pipelined TMEM drain + constant-bank bias (on top of the four producers)
+# A/B: VGG11 stem pool epilogue: tile coordinates carried forward (no per-tile divisions)
 for L in abtest/libhapi_base.so paper_2210_08650_b200/libhapi.so; do
   HAPI_LIB=$L timeout 300 python tools/outhash.py vgg11_s21_b256 2>&1 | tail -2
 done
